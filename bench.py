@@ -1,0 +1,408 @@
+"""Benchmark of the B200 alias-table pipeline (driver contract: one JSON line).
+
+Workload (BASELINE.json metric "alias-table build items/s at N=1e9 and
+samples/s (1/2/4/8 B200) vs HBM roofline"; configs C4 + C5):
+  * synthetic weights: gen_uniform(N=1e9, RngStream(seed=1)) cast to float32,
+    generated on every GPU (identical replicas, already resident in HBM);
+  * one step = build the N=1e9 alias table from the resident weights
+    (psa_construct -> 3 kernels) + M = 1e11 batched/sectioned draws (S=2^14,
+    RngStream(seed=1, stream=7)) split over the ranks (strong scaling), drawn in
+    passes into a reused 8 GB output buffer;
+  * value = total samples / max-over-ranks sampling time; the build is
+    reported beside it as items/s with its own roofline.
+Inputs (4 GB weights, 8 GB table, 8 GB output) exceed the 126 MB L2, so no
+explicit flush is needed between steps.
+
+`--impl reference` times the reference algorithm on the host cores instead:
+the C restatement in oracle/ (the reference is Python and cannot be compiled
+into oracle/_ref), on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "alias-table build items/s at N=1e9 and samples/s (1/2/4/8 B200) vs HBM roofline"
+UNIT = "samples/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=float, default=1e9)
+    ap.add_argument("--samples", type=float, default=1e11, help="draws per step, whole job")
+    ap.add_argument("--section", type=int, default=1 << 14)
+    ap.add_argument("--rng", default="philox4x32", choices=["philox4x32", "reference"])
+    ap.add_argument("--dtype", default="float32", choices=["float32", "float64"])
+    ap.add_argument("--e2e-samples", type=float, default=5e8)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-n", type=float, default=1e7)
+    ap.add_argument("--cpu-samples", type=float, default=5e7)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference algorithm (oracle restatement) on host cores
+# ---------------------------------------------------------------------------
+def cpu_baseline(n_items: int, n_samples: int, section: int, threads: int):
+    import oracle as O
+
+    r = np.random.default_rng(1)
+    w = r.random(n_items).astype(np.float32).astype(np.float64) + 0.0
+    w[w == 0.0] = 0.5
+    _, tot = O.make_weight_set(w)
+    t0 = time.perf_counter()
+    t = O.psa_construct(w, tot, s=max(64, n_items // 65536), workers=threads)
+    t_build = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.sectioned_sample(t, section, n_samples, 1, 7, 0)
+    t_sec = time.perf_counter() - t0
+    m_naive = n_samples
+    t0 = time.perf_counter()
+    O.sample_batch(t, m_naive, 1, 7, 0, workers=min(threads, 16))
+    t_naive = time.perf_counter() - t0
+    return {
+        "build_items_per_s": n_items / t_build,
+        "sectioned_samples_per_s": n_samples / t_sec,
+        "naive_samples_per_s": m_naive / t_naive,
+        "build_s": t_build, "sectioned_s": t_sec, "naive_s": t_naive,
+    }
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    n_items, n_samples = int(a.cpu_n), int(a.cpu_samples)
+    vals = []
+    detail = None
+    for i in range(a.warmup + a.steps):
+        d = cpu_baseline(n_items, n_samples, a.section, threads)
+        if i >= a.warmup:
+            vals.append(max(d["sectioned_samples_per_s"], d["naive_samples_per_s"]))
+            detail = d
+    v = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"reference CPU path (oracle/ C restatement of aliaskit): "
+                               f"psa_construct N={n_items:.0e} + sectioned (serial, S={a.section}) "
+                               f"and naive (<=16 workers) sampling of {n_samples:.0e} draws; "
+                               "value = the faster sampler",
+                   "build_items_per_s": detail["build_items_per_s"],
+                   "sectioned_samples_per_s": detail["sectioned_samples_per_s"],
+                   "naive_samples_per_s": detail["naive_samples_per_s"]},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"N={n_items:.0e} float32-upcast uniform weights, {n_samples:.0e} draws"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2106_12270_b200 as ak
+    from paper_2106_12270_b200 import _lib
+    from paper_2106_12270_b200 import distributed as D
+    from paper_2106_12270_b200.sample import sectioned_sample_into
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    N = int(a.n)
+    M = int(a.samples)
+    S = a.section
+    dtype = torch.float32 if a.dtype == "float32" else torch.float64
+    b_w = 4 if dtype == torch.float32 else 8
+    b_row = b_w + 4
+    peak, peak_kind = measured_peaks()
+
+    # synthetic input, resident in HBM (identical replica on every rank)
+    ws = ak.gen_uniform(N, ak.RngStream(seed=1), dtype=dtype, device=dev)
+    torch.cuda.synchronize()
+    table = ak.psa_construct(ws)  # allocation + warm path
+    r0 = ak.RngStream(seed=1, stream=7)
+
+    # sampling pass plan: this rank's contiguous section run, cut into passes
+    asg = ak.assign_sections(N, S, M, r0.seed, r0.stream)
+    S_eff = asg.section_size
+    first, count, out_off, draws = D.section_shard(asg.counts, rank, world)
+    counts_d = torch.from_numpy(asg.counts).to(dev)
+    offs = np.concatenate([[0], np.cumsum(asg.counts)[:-1]])
+    offs_d = torch.from_numpy(offs).to(dev)
+    cap = 1 << 30 if M >= (1 << 30) else max(M, 1)
+    out = torch.empty(cap, dtype=torch.int64, device=dev)
+    passes = []
+    j = first
+    end = first + count
+    while j < end:
+        k, tot = j, 0
+        while k < end and tot + int(asg.counts[k]) <= cap:
+            tot += int(asg.counts[k])
+            k += 1
+        if k == j:
+            raise RuntimeError("a single section exceeds the output buffer")
+        passes.append((j, k - j, int(offs[j]), tot))
+        j = k
+    rng_mode = a.rng
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+
+    def step(record):
+        e0, e1, e2 = ev(), ev(), ev()
+        e0.record()
+        ak.pack.build_table(ws, table)
+        e1.record()
+        # host part of sectioned_sample (bit-exact binomial assignment) is
+        # inside the sampling interval, as in the reference
+        ak.assign_sections(N, S, M, r0.seed, r0.stream)
+        for (f, c, o, _) in passes:
+            sectioned_sample_into(table, S_eff, counts_d, offs_d, f, c, r0, out, o, rng_mode)
+        e2.record()
+        if record is not None:
+            record.append((e0, e1, e2))
+
+    for _ in range(a.warmup):
+        step(None)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    recs = []
+    w0 = time.perf_counter()
+    for _ in range(a.steps):
+        step(recs)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    clocks = clk.stop()
+    t_build = sum(e0.elapsed_time(e1) for e0, e1, _ in recs) / 1e3
+    t_samp = sum(e1.elapsed_time(e2) for _, e1, e2 in recs) / 1e3
+    t_step = sum(e0.elapsed_time(e2) for e0, _, e2 in recs) / 1e3
+    tt = torch.tensor([t_build, t_samp, t_step], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_build, t_samp, t_step = (float(x) for x in tt.tolist())
+
+    # per-kernel device times of one extra build and one sampling pass
+    def time_launch(fn, reps=3):
+        ts = []
+        for _ in range(reps):
+            s0, s1 = ev(), ev()
+            s0.record()
+            fn()
+            s1.record()
+            torch.cuda.synchronize()
+            ts.append(s0.elapsed_time(s1) / 1e3)
+        return statistics.median(ts)
+
+    f0, c0, o0, d0 = passes[0]
+    t_pass = time_launch(lambda: sectioned_sample_into(table, S_eff, counts_d, offs_d, f0, c0, r0, out, o0, rng_mode))
+    pass_bytes = d0 * 8 + c0 * S_eff * b_row
+    t_build1 = time_launch(lambda: ak.pack.build_table(ws, table))
+    build_bytes = N * (2 * b_w + b_row)
+    # reference-RNG (bit-exact mode) throughput of the same pass, for context
+    t_pass_ref = time_launch(lambda: sectioned_sample_into(table, S_eff, counts_d, offs_d, f0, c0, r0, out, o0, "reference"))
+
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                ps = json.load(f)
+            k = ps.get("kernels", {}).get("k_sample_sectioned")
+            if k and k.get("dram_bytes") and k.get("draws"):
+                traffic = k["dram_bytes"] / k["draws"] * d0
+        except Exception:
+            traffic = None
+
+    # end-to-end through the public API with host buffers (per rank)
+    e2e = None
+    if not a.no_e2e:
+        Me = int(a.e2e_samples)
+        off_e, cnt_e = D.naive_shard(Me, rank, world)
+        w_host = ws.weights.cpu().pin_memory()
+        o_host = torch.empty(cnt_e, dtype=torch.int64).pin_memory()
+        times = []
+        for i in range(a.e2e_steps + 1):
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            s0 = time.perf_counter()
+            wd = w_host.to(dev, non_blocking=True)
+            wse = ak.make_weight_set(wd)
+            te = ak.psa_construct(wse)
+            asg_e = ak.assign_sections(N, S, Me, 1, 7)
+            f_e, c_e, oo_e, dr_e = D.section_shard(asg_e.counts, rank, world)
+            cd = torch.from_numpy(asg_e.counts).to(dev)
+            od = torch.from_numpy(np.concatenate([[0], np.cumsum(asg_e.counts)[:-1]])).to(dev)
+            oe = torch.empty(dr_e, dtype=torch.int64, device=dev)
+            sectioned_sample_into(te, asg_e.section_size, cd, od, f_e, c_e, ak.RngStream(1, 7), oe, oo_e, rng_mode)
+            o_host[:dr_e].copy_(oe, non_blocking=True)
+            torch.cuda.synchronize()
+            el = time.perf_counter() - s0
+            del wd, wse, te, oe
+            tt2 = torch.tensor([el], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(tt2, op=dist.ReduceOp.MAX)
+            if i > 0:
+                times.append(float(tt2.item()))
+        e2e = {"value": Me / statistics.median(times), "unit": UNIT,
+               "h2d_bytes_per_step": int(N * b_w), "d2h_bytes_per_step": int(cnt_e * 8),
+               "path": "pinned host f32 weights -> make_weight_set -> psa_construct -> "
+                       "sectioned_sample -> pinned host int64 samples",
+               "samples_per_step": Me, "s_per_step": statistics.median(times)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        threads = os.cpu_count() or 1
+        d = cpu_baseline(int(a.cpu_n), int(a.cpu_samples), S, threads)
+        v = max(d["sectioned_samples_per_s"], d["naive_samples_per_s"])
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"oracle/ C restatement: N={a.cpu_n:.0e} build + {a.cpu_samples:.0e} draws "
+                         f"(sectioned serial / naive <=16 threads; faster reported)",
+               "build_items_per_s": d["build_items_per_s"],
+               "sectioned_samples_per_s": d["sectioned_samples_per_s"],
+               "naive_samples_per_s": d["naive_samples_per_s"]}
+
+    if rank == 0:
+        value = M * a.steps / t_samp
+        ach = pass_bytes / t_pass / 1e9
+        bach = build_bytes / t_build1 / 1e9
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": t_step / a.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"C4+C5: N={N:.0e} {a.dtype} table (gen_uniform seed=1) built per step, "
+                                   f"then {M:.0e} sectioned draws (S={S}, RngStream(1,7), rng={rng_mode}) "
+                                   f"split over {world} GPU(s)",
+                       "n": N, "samples": M, "section_size": S, "rng": rng_mode,
+                       "weights_dtype": a.dtype, "parallelism": f"replicas x{world}, section-range shards",
+                       "l2": "inputs (weights 4 GB, table 8 GB, output 8 GB) exceed L2; no flush needed",
+                       "passes_per_step": len(passes)},
+            "build": {"items_per_s": N * a.steps / t_build, "ms": t_build / a.steps * 1e3,
+                      "roofline": {"bound": "hbm", "achieved": bach, "peak": peak, "unit": "GB/s",
+                                   "frac": bach / peak, "algorithmic_bytes": build_bytes,
+                                   "bytes_per_item": 2 * b_w + b_row}},
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                         "frac": ach / peak, "traffic": traffic, "kernel": "k_sample_sectioned",
+                         "algorithmic_bytes_per_launch": pass_bytes, "peak_kind": peak_kind},
+            "sampling_reference_rng": {"samples_per_s": d0 / t_pass_ref,
+                                       "frac": pass_bytes / t_pass_ref / 1e9 / peak},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": a.steps * (3 + len(passes)),
+            "clocks": clocks,
+            "wall_s_timed_region": wall,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    return run_ours(a)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,752 @@
+// ak_partition.cu — the structured PSA path in the reference's own layout:
+//
+//   ak_partition           partition_items (partition.py:106-131)
+//   ak_split_plan          compute_split_plan (split.py:94-104, 52-88)
+//   ak_partial_pary_search partial_pary_search (split.py:190-213)
+//   ak_pack_sections       pack_section / chunked_pack_section (pack.py:30-232)
+//
+// These exist so the reference's step-by-step API (partition -> plan -> pack)
+// runs on the device with the reference's semantics; the split and pack
+// kernels are bit-identical to the reference on the same inputs.  The fast
+// construction path is the fused builder in ak_build.cu.
+#include "ak_common.cuh"
+
+namespace {
+
+constexpr int PT_THREADS = 256;
+constexpr int PT_V = 8;
+constexpr int PT_TILE = PT_THREADS * PT_V;
+
+// ---------------------------------------------------------------------------
+// partition: tile counts + double-double sums, scan, scatter
+// ---------------------------------------------------------------------------
+struct PartAgg {
+    u64 nl;
+    dd sl, sh;
+};
+
+template <typename T>
+__device__ __forceinline__ void load_tile(const T *w, u64 n, u64 base, double v[PT_V], bool ok[PT_V])
+{
+#pragma unroll
+    for (int k = 0; k < PT_V; ++k) {
+        u64 i = base + (u64)threadIdx.x * PT_V + k;
+        ok[k] = i < n;
+        v[k] = ok[k] ? (double)w[i] : 0.0;
+    }
+}
+
+__device__ __forceinline__ dd shfl_up_dd(dd x, int d)
+{
+    return dd_make(shfl_up_d(x.hi, d), shfl_up_d(x.lo, d));
+}
+
+// block exclusive scan of (count, dd, dd); returns block totals in *tot
+__device__ void block_scan3(u64 c, dd a, dd b, u64 &c_ex, dd &a_ex, dd &b_ex, u64 *ctot, dd *atot,
+                            dd *btot)
+{
+    __shared__ u64 sc[PT_THREADS / 32];
+    __shared__ dd sa[PT_THREADS / 32], sb[PT_THREADS / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    u64 ci = c;
+    dd ai = a, bi = b;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        u64 cu = __shfl_up_sync(0xffffffffu, ci, d);
+        dd au = shfl_up_dd(ai, d), bu = shfl_up_dd(bi, d);
+        if (lane >= d) {
+            ci += cu;
+            ai = dd_add(au, ai);
+            bi = dd_add(bu, bi);
+        }
+    }
+    if (lane == 31) {
+        sc[wid] = ci;
+        sa[wid] = ai;
+        sb[wid] = bi;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = PT_THREADS / 32;
+        u64 wc = lane < nw ? sc[lane] : 0;
+        dd wa = lane < nw ? sa[lane] : dd_make(0.0), wb = lane < nw ? sb[lane] : dd_make(0.0);
+#pragma unroll
+        for (int d = 1; d < nw; d <<= 1) {
+            u64 cu = __shfl_up_sync(0xffffffffu, wc, d);
+            dd au = shfl_up_dd(wa, d), bu = shfl_up_dd(wb, d);
+            if (lane >= d) {
+                wc += cu;
+                wa = dd_add(au, wa);
+                wb = dd_add(bu, wb);
+            }
+        }
+        if (lane < nw) {
+            sc[lane] = wc;
+            sa[lane] = wa;
+            sb[lane] = wb;
+        }
+    }
+    __syncthreads();
+    u64 wbase_c = wid ? sc[wid - 1] : 0;
+    dd wbase_a = wid ? sa[wid - 1] : dd_make(0.0), wbase_b = wid ? sb[wid - 1] : dd_make(0.0);
+    // exclusive within warp = inclusive - own
+    u64 ce = __shfl_up_sync(0xffffffffu, ci, 1);
+    dd ae = shfl_up_dd(ai, 1), be = shfl_up_dd(bi, 1);
+    if (lane == 0) {
+        ce = 0;
+        ae = dd_make(0.0);
+        be = dd_make(0.0);
+    }
+    c_ex = wbase_c + ce;
+    a_ex = dd_add(wbase_a, ae);
+    b_ex = dd_add(wbase_b, be);
+    *ctot = sc[PT_THREADS / 32 - 1];
+    *atot = sa[PT_THREADS / 32 - 1];
+    *btot = sb[PT_THREADS / 32 - 1];
+    __syncthreads();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(PT_THREADS) k_part_tiles(const T *__restrict__ w, u64 n,
+                                                           double avg, PartAgg *__restrict__ agg)
+{
+    double v[PT_V];
+    bool ok[PT_V];
+    const u64 base = (u64)blockIdx.x * PT_TILE;
+    load_tile(w, n, base, v, ok);
+    u64 c = 0;
+    dd a = dd_make(0.0), b = dd_make(0.0);
+#pragma unroll
+    for (int k = 0; k < PT_V; ++k) {
+        if (!ok[k]) continue;
+        if (v[k] <= avg) {
+            ++c;
+            a = dd_add_d(a, v[k]);
+        } else {
+            b = dd_add_d(b, v[k]);
+        }
+    }
+    u64 ce, ct;
+    dd ae, be, at, bt;
+    block_scan3(c, a, b, ce, ae, be, &ct, &at, &bt);
+    if (threadIdx.x == 0) agg[blockIdx.x] = PartAgg{ct, at, bt};
+}
+
+// exclusive scan over tile aggregates, single block (tiles <= a few 1e5)
+__global__ void __launch_bounds__(PT_THREADS) k_part_scan(PartAgg *__restrict__ agg, u64 ntiles,
+                                                          PartAgg *__restrict__ total)
+{
+    __shared__ PartAgg carry;
+    if (threadIdx.x == 0) carry = PartAgg{0, dd_make(0.0), dd_make(0.0)};
+    __syncthreads();
+    for (u64 b0 = 0; b0 < ntiles; b0 += PT_THREADS) {
+        u64 i = b0 + threadIdx.x;
+        PartAgg x = i < ntiles ? agg[i] : PartAgg{0, dd_make(0.0), dd_make(0.0)};
+        u64 ce, ct;
+        dd ae, be, at, bt;
+        block_scan3(x.nl, x.sl, x.sh, ce, ae, be, &ct, &at, &bt);
+        PartAgg cr = carry;
+        if (i < ntiles) agg[i] = PartAgg{cr.nl + ce, dd_add(cr.sl, ae), dd_add(cr.sh, be)};
+        __syncthreads();
+        if (threadIdx.x == 0) carry = PartAgg{cr.nl + ct, dd_add(cr.sl, at), dd_add(cr.sh, bt)};
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(PT_THREADS) k_part_scatter(
+    const T *__restrict__ w, u64 n, double avg, const PartAgg *__restrict__ ex, i64 *l_idx, T *l_w,
+    i64 *h_idx, T *h_w, double *lpre, double *hpre, const PartAgg *__restrict__ total)
+{
+    double v[PT_V];
+    bool ok[PT_V];
+    const u64 base = (u64)blockIdx.x * PT_TILE;
+    load_tile(w, n, base, v, ok);
+    u64 c = 0;
+    dd a = dd_make(0.0), b = dd_make(0.0);
+#pragma unroll
+    for (int k = 0; k < PT_V; ++k) {
+        if (!ok[k]) continue;
+        if (v[k] <= avg) {
+            ++c;
+            a = dd_add_d(a, v[k]);
+        } else {
+            b = dd_add_d(b, v[k]);
+        }
+    }
+    u64 ce, ct;
+    dd ae, be, at, bt;
+    block_scan3(c, a, b, ce, ae, be, &ct, &at, &bt);
+    const PartAgg t = ex[blockIdx.x];
+    u64 kl = t.nl + ce;                         // lights before this thread's items
+    u64 kh = base + (u64)threadIdx.x * PT_V - kl;  // heavies before
+    dd L = dd_add(t.sl, ae), H = dd_add(t.sh, be);
+#pragma unroll
+    for (int k = 0; k < PT_V; ++k) {
+        if (!ok[k]) continue;
+        u64 i = base + (u64)threadIdx.x * PT_V + k;
+        if (v[k] <= avg) {
+            l_idx[kl] = (i64)i + 1;
+            l_w[kl] = (T)v[k];
+            L = dd_add_d(L, v[k]);
+            lpre[kl + 1] = L.hi + L.lo;
+            ++kl;
+        } else {
+            h_idx[kh] = (i64)i + 1;
+            h_w[kh] = (T)v[k];
+            H = dd_add_d(H, v[k]);
+            hpre[kh + 1] = H.hi + H.lo;
+            ++kh;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        lpre[0] = 0.0;
+        hpre[0] = 0.0;
+    }
+    (void)total;
+}
+
+// ---------------------------------------------------------------------------
+// split plan (split.py:52-88)
+// ---------------------------------------------------------------------------
+struct PlanArgs {
+    const double *lpre, *hpre;
+    i64 nl, nh;
+    u64 n_total, s;
+    double avg;
+    i64 *lc, *hc;
+    double *sp;
+};
+
+__device__ __forceinline__ i64 boundary_n(u64 i, u64 n, u64 s)
+{
+    return (i64)(((unsigned __int128)i * n) / s);
+}
+
+template <typename T>
+__device__ __forceinline__ void plan_finish(const PlanArgs &A, const T *h_w, u64 i, i64 ni,
+                                            double cap, i64 h)
+{
+    i64 l = ni - h;
+    double taken = cap - (A.lpre[l] + A.hpre[h]);
+    double sp = 0.0;
+    if (h < A.nh && taken > 0.0) {
+        sp = (double)h_w[h] - taken;
+        if (sp < 0.0) sp = 0.0;
+    }
+    A.lc[i] = l;
+    A.hc[i] = h;
+    A.sp[i] = sp;
+}
+
+template <typename T>
+__global__ void k_plan_binary(PlanArgs A, const T *__restrict__ h_w)
+{
+    u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) {
+        A.lc[0] = 0;
+        A.hc[0] = 0;
+        A.sp[0] = 0.0;
+        A.lc[A.s] = A.nl;
+        A.hc[A.s] = A.nh;
+        A.sp[A.s] = 0.0;
+    }
+    if (i < 1 || i >= A.s) return;
+    i64 ni = boundary_n(i, A.n_total, A.s);
+    double cap = (double)ni * A.avg;
+    i64 lo = ni - A.nl;
+    if (lo < 0) lo = 0;
+    i64 hi = ni < A.nh ? ni : A.nh;
+    i64 best = lo, a = lo, b = hi;
+    while (a <= b) {
+        i64 mid = (a + b) >> 1;
+        if (A.lpre[ni - mid] + A.hpre[mid] <= cap) {
+            best = mid;
+            a = mid + 1;
+        } else {
+            b = mid - 1;
+        }
+    }
+    plan_finish(A, h_w, i, ni, cap, best);
+}
+
+// Batched split (the paper's generalised parallel search): a CTA owns RUN
+// consecutive boundaries.  Warp 0 locates the two end states with 32-ary
+// probes (each round 32 lanes test 32 evenly spaced h), which bounds every
+// interior boundary's h range; the H and L prefix windows covering that range
+// are then staged in shared memory and each thread finishes its boundary
+// with a binary search there.
+constexpr int PLAN_RUN = 256;
+constexpr int PLAN_SMEM_DOUBLES = 12 * 1024;  // 96 KB of staged prefix values
+
+__device__ i64 pary_boundary(const PlanArgs &A, i64 ni, double cap)
+{
+    // greatest h in [lo, hi] with L[ni-h] + H[h] <= cap, 32-ary then finish
+    const int lane = threadIdx.x & 31;
+    i64 lo = ni - A.nl;
+    if (lo < 0) lo = 0;
+    i64 hi = ni < A.nh ? ni : A.nh;
+    // invariant: pred(lo) true or lo is the range floor; pred(hi+1) false
+    i64 a = lo, b = hi;  // answer in [a, b]
+    while (b - a > 32) {
+        i64 width = b - a;
+        i64 h = a + (i64)(((__int128)(lane + 1) * width) / 33);
+        bool pr = A.lpre[ni - h] + A.hpre[h] <= cap;
+        unsigned m = __ballot_sync(0xffffffffu, pr);
+        // pred is monotone (true then false): count of true probes
+        int t = __popc(m);
+        i64 na = t ? a + (i64)(((__int128)t * width) / 33) : a;
+        i64 nb = t < 32 ? a + (i64)(((__int128)(t + 1) * width) / 33) - 1 : b;
+        a = na;
+        b = nb;
+    }
+    // finish: lanes test a..b (<= 33 values)
+    i64 h = a + lane;
+    bool pr = h <= b && (A.lpre[ni - h] + A.hpre[h] <= cap);
+    unsigned m = __ballot_sync(0xffffffffu, pr);
+    i64 best = lo;
+    if (m) best = a + 31 - __clz(m);  // greatest true
+    // b - a can be 32 (33 values): test the last one separately
+    if (b - a == 32) {
+        bool pb = A.lpre[ni - b] + A.hpre[b] <= cap;
+        if (pb) best = b;
+    }
+    return best;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(PLAN_RUN) k_plan_batched(PlanArgs A, const T *__restrict__ h_w)
+{
+    __shared__ i64 ends[2];
+    extern __shared__ double stage[];
+    const u64 i0 = 1 + (u64)blockIdx.x * PLAN_RUN;
+    if (i0 >= A.s) return;
+    u64 i1 = i0 + PLAN_RUN - 1;  // inclusive
+    if (i1 > A.s - 1) i1 = A.s - 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        A.lc[0] = 0;
+        A.hc[0] = 0;
+        A.sp[0] = 0.0;
+        A.lc[A.s] = A.nl;
+        A.hc[A.s] = A.nh;
+        A.sp[A.s] = 0.0;
+    }
+    if (threadIdx.x < 64) {
+        const int which = threadIdx.x >> 5;  // warp 0: first, warp 1: last
+        u64 i = which ? i1 : i0;
+        i64 ni = boundary_n(i, A.n_total, A.s);
+        i64 h = pary_boundary(A, ni, (double)ni * A.avg);
+        if ((threadIdx.x & 31) == 0) ends[which] = h;
+    }
+    __syncthreads();
+    const i64 hA = ends[0], hB = ends[1];
+    const i64 nA = boundary_n(i0, A.n_total, A.s), nB = boundary_n(i1, A.n_total, A.s);
+    // windows: H[hA .. hB], L[nA - hB .. nB - hA]
+    const i64 hlen = hB - hA + 1;
+    const i64 l0 = nA - hB, llen = (nB - hA) - l0 + 1;
+    const bool staged = hlen > 0 && llen > 0 && hlen + llen <= PLAN_SMEM_DOUBLES;
+    if (staged) {
+        for (i64 t = threadIdx.x; t < hlen; t += blockDim.x) stage[t] = A.hpre[hA + t];
+        for (i64 t = threadIdx.x; t < llen; t += blockDim.x) stage[hlen + t] = A.lpre[l0 + t];
+    }
+    __syncthreads();
+    const u64 i = i0 + threadIdx.x;
+    if (i > i1) return;
+    i64 ni = boundary_n(i, A.n_total, A.s);
+    double cap = (double)ni * A.avg;
+    i64 lo = ni - A.nl;
+    if (lo < 0) lo = 0;
+    i64 hi = ni < A.nh ? ni : A.nh;
+    if (lo < hA) lo = hA;
+    if (hi > hB) hi = hB;
+    i64 best = lo, a = lo, b = hi;
+    while (a <= b) {
+        i64 mid = (a + b) >> 1;
+        double L = staged ? stage[hlen + (ni - mid - l0)] : A.lpre[ni - mid];
+        double H = staged ? stage[mid - hA] : A.hpre[mid];
+        if (L + H <= cap) {
+            best = mid;
+            a = mid + 1;
+        } else {
+            b = mid - 1;
+        }
+    }
+    plan_finish(A, h_w, i, ni, cap, best);
+}
+
+// ---------------------------------------------------------------------------
+// partial_pary_search (split.py:140-213)
+// ---------------------------------------------------------------------------
+__global__ void k_check_sorted(const double *a, u64 n, int *flag)
+{
+    u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x + 1; i < n; i += stride)
+        if (a[i] < a[i - 1]) atomicOr(flag, 1);
+}
+
+// _contract_range (split.py:157-187) by one warp: lanes evaluate the p
+// pivots of a round in parallel; the reductions reproduce the sequential
+// "last pivot < qmin" / "first pivot > qmax" picks exactly.
+__global__ void k_contract(const double *hay, u64 n, const double *q, u64 m, int p, i64 *ab)
+{
+    const int lane = threadIdx.x;
+    const double qmin = q[0], qmax = q[m - 1];
+    i64 a = 0, b = (i64)n;
+    while (b - a > p) {
+        i64 width = b - a;
+        i64 gs = -1, ls = -1, t_gs = -1, t_ls = -1;
+        for (int t0 = 0; t0 < p; t0 += 32) {
+            int t = t0 + lane;
+            int cls = 0;  // 1: < qmin, 2: > qmax
+            i64 s = 0;
+            if (t < p) {
+                s = a + (i64)t * (width - 1) / (p - 1);
+                double v = hay[s];
+                cls = v < qmin ? 1 : (v > qmax ? 2 : 0);
+            }
+            unsigned mlt = __ballot_sync(0xffffffffu, cls == 1);
+            unsigned mgt = __ballot_sync(0xffffffffu, cls == 2);
+            if (mlt) {  // greatest t with v < qmin (pivots are sorted by t)
+                int l = 31 - __clz(mlt);
+                t_gs = t0 + l;
+                gs = __shfl_sync(0xffffffffu, s, l);
+            }
+            if (mgt && ls < 0) {  // least t with v > qmax
+                int l = __ffs(mgt) - 1;
+                t_ls = t0 + l;
+                ls = __shfl_sync(0xffffffffu, s, l);
+            }
+        }
+        i64 na = gs >= 0 ? gs + 1 : a;
+        i64 nb = ls >= 0 ? ls : b;
+        i64 band = (t_ls >= 0 ? t_ls : p) - (t_gs >= 0 ? t_gs : -1);
+        a = na;
+        b = nb;
+        if (band >= p - 2 || 2 * (b - a) > width) break;
+    }
+    if (lane == 0) {
+        ab[0] = a;
+        ab[1] = b;
+    }
+}
+
+__global__ void k_lower_bound(const double *hay, const double *q, u64 m, const i64 *ab, i64 *out)
+{
+    u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    i64 lo = ab[0], hi = ab[1];
+    double x = q[i];
+    while (lo < hi) {
+        i64 mid = (lo + hi) >> 1;
+        if (hay[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    out[i] = lo;
+}
+
+// ---------------------------------------------------------------------------
+// pack sections (pack.py:30-159)
+// ---------------------------------------------------------------------------
+template <typename T>
+struct PackArgs {
+    const i64 *l_idx;
+    const T *l_w;
+    const i64 *h_idx;
+    const T *h_w;
+    i64 nl, nh;
+    const i64 *lc, *hc;
+    const double *sp;
+    u64 s, sec_first, sec_last;
+    double avg;
+    typename RowOf<T>::type *rows;
+    double *out_spills;
+};
+
+template <typename T>
+__device__ __forceinline__ void put_row(typename RowOf<T>::type *rows, i64 it, double tw, i64 alias,
+                                        double avg)
+{
+    typename RowOf<T>::type r;
+    r.tw = tw_store<T>(tw, avg);
+    r.alias = (decltype(r.alias))alias;
+    rows[it - 1] = r;
+}
+
+// _pack_range (pack.py:30-71): one thread per section, the reference sweep
+template <typename T>
+__global__ void k_pack_plain(PackArgs<T> A)
+{
+    u64 sec = A.sec_first + (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (sec > A.sec_last) return;
+    const i64 nh = A.nh;
+    i64 la = A.lc[sec - 1], lb = A.lc[sec], ha = A.hc[sec - 1], hb = A.hc[sec];
+    double spill_in = A.sp[sec - 1];
+    i64 k = la, j = ha;
+    double w = j < nh ? (spill_in > 0.0 ? spill_in : (double)A.h_w[j]) : 0.0;
+    while (k < lb || j < hb) {
+        if (j < nh && w > A.avg && k < lb) {
+            i64 it = A.l_idx[k];
+            double lw = (double)A.l_w[k];
+            put_row<T>(A.rows, it, lw, A.h_idx[j], A.avg);
+            w += lw - A.avg;
+            k++;
+        } else if (j < hb) {
+            i64 it = A.h_idx[j];
+            if (j + 1 < nh) {
+                put_row<T>(A.rows, it, w, A.h_idx[j + 1], A.avg);
+                w += (double)A.h_w[j + 1] - A.avg;
+            } else {
+                put_row<T>(A.rows, it, w, it, A.avg);
+                w = 0.0;
+            }
+            j++;
+        } else {
+            i64 it = A.l_idx[k];
+            put_row<T>(A.rows, it, (double)A.l_w[k], it, A.avg);
+            k++;
+        }
+    }
+    if (A.out_spills) A.out_spills[sec - A.sec_first] = j < nh ? w : 0.0;
+}
+
+// _chunked_pack_range (pack.py:74-159): one warp per section.  The warp
+// copies light and heavy chunks of `cap` entries coalesced into its shared
+// memory slice, refilling a buffer once more than two thirds of it has been
+// consumed (heavy staging extends to hb+1); lane 0 runs the sweep from shared
+// memory.  Arithmetic is the plain sweep's, so the rows are bit-identical.
+constexpr int CH_WARPS = 4;
+
+template <typename T>
+__global__ void __launch_bounds__(CH_WARPS * 32) k_pack_chunked(PackArgs<T> A, int cap)
+{
+    extern __shared__ unsigned char ch_smem[];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const u64 sec = A.sec_first + (u64)blockIdx.x * CH_WARPS + wid;
+    // per-warp slice: sl_idx, sh_idx (i64) then sl_w, sh_w (double)
+    i64 *sl_idx = (i64 *)(ch_smem + (size_t)wid * cap * 32);
+    i64 *sh_idx = sl_idx + cap;
+    double *sl_w = (double *)(sh_idx + cap);
+    double *sh_w = sl_w + cap;
+    if (sec > A.sec_last) return;
+    const i64 nh = A.nh;
+    const i64 la = A.lc[sec - 1], lb = A.lc[sec], ha = A.hc[sec - 1], hb = A.hc[sec];
+    const double spill_in = A.sp[sec - 1];
+    const i64 hext = hb + 1 < nh ? hb + 1 : nh;
+    i64 k = la, j = ha;
+    i64 lw_lo = la, lw_hi = la, hw_lo = ha, hw_hi = ha;
+    double w = 0.0;
+    auto stage_l = [&](i64 from) {
+        lw_lo = from;
+        lw_hi = from + cap < lb ? from + cap : lb;
+        for (i64 t = lw_lo + lane; t < lw_hi; t += 32) {
+            sl_idx[t - lw_lo] = A.l_idx[t];
+            sl_w[t - lw_lo] = (double)A.l_w[t];
+        }
+        __syncwarp();
+    };
+    auto stage_h = [&](i64 from) {
+        hw_lo = from;
+        hw_hi = from + cap < hext ? from + cap : hext;
+        for (i64 t = hw_lo + lane; t < hw_hi; t += 32) {
+            sh_idx[t - hw_lo] = A.h_idx[t];
+            sh_w[t - hw_lo] = (double)A.h_w[t];
+        }
+        __syncwarp();
+    };
+    if (j < nh) {
+        if (spill_in > 0.0) w = spill_in;
+        else {
+            stage_h(j);
+            w = sh_w[0];
+        }
+    }
+    // every lane runs the (uniform) control flow so refills stay warp-wide;
+    // only lane 0 writes rows.
+    while (k < lb || j < hb) {
+        if (k < lb && (k >= lw_hi || 3 * (k - lw_lo) > 2 * (i64)cap)) stage_l(k);
+        if (j < hext && (j >= hw_hi || (hw_hi < hext && 3 * ((j + 1) - hw_lo) > 2 * (i64)cap)))
+            stage_h(j);
+        if (j < nh && w > A.avg && k < lb) {
+            i64 it = sl_idx[k - lw_lo];
+            double lw = sl_w[k - lw_lo];
+            if (lane == 0) put_row<T>(A.rows, it, lw, sh_idx[j - hw_lo], A.avg);
+            w += lw - A.avg;
+            k++;
+        } else if (j < hb) {
+            i64 it = sh_idx[j - hw_lo];
+            if (j + 1 < nh) {
+                if (lane == 0) put_row<T>(A.rows, it, w, sh_idx[j + 1 - hw_lo], A.avg);
+                w += sh_w[j + 1 - hw_lo] - A.avg;
+            } else {
+                if (lane == 0) put_row<T>(A.rows, it, w, it, A.avg);
+                w = 0.0;
+            }
+            j++;
+        } else {
+            i64 it = sl_idx[k - lw_lo];
+            if (lane == 0) put_row<T>(A.rows, it, sl_w[k - lw_lo], it, A.avg);
+            k++;
+        }
+    }
+    if (lane == 0 && A.out_spills) A.out_spills[sec - A.sec_first] = j < nh ? w : 0.0;
+}
+
+template <typename T>
+int run_partition(const void *wv, u64 n, double avg, i64 *l_idx, void *l_w, i64 *h_idx, void *h_w,
+                  double *lpre, double *hpre, u64 *nl_out, u64 *nh_out, void *ws,
+                  cudaStream_t st)
+{
+    const T *w = (const T *)wv;
+    const u64 tiles = (n + PT_TILE - 1) / PT_TILE;
+    PartAgg *agg = (PartAgg *)ws;
+    PartAgg *tot = agg + tiles;
+    k_part_tiles<T><<<(unsigned)tiles, PT_THREADS, 0, st>>>(w, n, avg, agg);
+    AK_LAUNCH_CHECK("k_part_tiles");
+    k_part_scan<<<1, PT_THREADS, 0, st>>>(agg, tiles, tot);
+    AK_LAUNCH_CHECK("k_part_scan");
+    k_part_scatter<T><<<(unsigned)tiles, PT_THREADS, 0, st>>>(w, n, avg, agg, l_idx, (T *)l_w,
+                                                              h_idx, (T *)h_w, lpre, hpre, tot);
+    AK_LAUNCH_CHECK("k_part_scatter");
+    PartAgg t;
+    AK_CUDA_TRY(cudaMemcpyAsync(&t, tot, sizeof(t), cudaMemcpyDeviceToHost, st));
+    AK_CUDA_TRY(cudaStreamSynchronize(st));
+    *nl_out = t.nl;
+    *nh_out = n - t.nl;
+    return AK_OK;
+}
+
+template <typename T>
+int run_plan(const double *lpre, u64 nl, const double *hpre, u64 nh, const void *h_w, u64 n_total,
+             u64 s, double avg, i64 *lc, i64 *hc, double *sp, int method, cudaStream_t st)
+{
+    PlanArgs A{lpre, hpre, (i64)nl, (i64)nh, n_total, s, avg, lc, hc, sp};
+    if (method == 0 || s < 2) {
+        u64 thr = s + 1;
+        k_plan_binary<T><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(A, (const T *)h_w);
+        AK_LAUNCH_CHECK("k_plan_binary");
+    } else {
+        u64 runs = (s - 1 + PLAN_RUN - 1) / PLAN_RUN;
+        size_t smem = PLAN_SMEM_DOUBLES * sizeof(double);
+        AK_CUDA_TRY(cudaFuncSetAttribute(k_plan_batched<T>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_plan_batched<T><<<(unsigned)runs, PLAN_RUN, smem, st>>>(A, (const T *)h_w);
+        AK_LAUNCH_CHECK("k_plan_batched");
+    }
+    return AK_OK;
+}
+
+template <typename T>
+int run_pack(const i64 *l_idx, const void *l_w, u64 nl, const i64 *h_idx, const void *h_w, u64 nh,
+             const i64 *lc, const i64 *hc, const double *sp, u64 s, u64 f, u64 l, double avg,
+             void *rows, double *out_spills, u32 cap, cudaStream_t st)
+{
+    PackArgs<T> A{l_idx, (const T *)l_w, h_idx, (const T *)h_w, (i64)nl, (i64)nh, lc, hc, sp, s,
+                  f, l, avg, (typename RowOf<T>::type *)rows, out_spills};
+    u64 cnt = l - f + 1;
+    if (cap == 0) {
+        k_pack_plain<T><<<(unsigned)((cnt + 127) / 128), 128, 0, st>>>(A);
+        AK_LAUNCH_CHECK("k_pack_plain");
+    } else {
+        // device staging capacity: the caller's chunk capacity, bounded by
+        // shared memory; the staging schedule never changes the arithmetic.
+        int c = cap > 512 ? 512 : (int)cap;
+        size_t smem = (size_t)CH_WARPS * c * 32;
+        AK_CUDA_TRY(cudaFuncSetAttribute(k_pack_chunked<T>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_pack_chunked<T><<<(unsigned)((cnt + CH_WARPS - 1) / CH_WARPS), CH_WARPS * 32, smem, st>>>(
+            A, c);
+        AK_LAUNCH_CHECK("k_pack_chunked");
+    }
+    return AK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t ak_partition_workspace_bytes(uint64_t n)
+{
+    u64 tiles = (n + PT_TILE - 1) / PT_TILE;
+    return (tiles + 2) * sizeof(PartAgg) + 256;
+}
+
+int ak_partition(const void *w, int dtype, uint64_t n, double avg, int64_t *l_idx, void *l_w,
+                 int64_t *h_idx, void *h_w, double *lprefix, double *hprefix, uint64_t *nl_out,
+                 uint64_t *nh_out, void *ws, size_t ws_bytes, void *stream)
+{
+    if (n == 0) return AK_ERR_EMPTY_INPUT;
+    if (ws_bytes < ak_partition_workspace_bytes(n)) return AK_ERR_WORKSPACE;
+    if (dtype == AK_F32)
+        return run_partition<float>(w, n, avg, l_idx, l_w, h_idx, h_w, lprefix, hprefix, nl_out,
+                                    nh_out, ws, ak_stream(stream));
+    if (dtype == AK_F64)
+        return run_partition<double>(w, n, avg, l_idx, l_w, h_idx, h_w, lprefix, hprefix, nl_out,
+                                     nh_out, ws, ak_stream(stream));
+    return AK_ERR_VALUE;
+}
+
+int ak_split_plan(const double *lprefix, uint64_t nl, const double *hprefix, uint64_t nh,
+                  const void *h_w, int dtype, uint64_t n_total, uint64_t s, double avg,
+                  int64_t *lcounts, int64_t *hcounts, double *spills, int method, void *stream)
+{
+    if (s < 1 || s > (n_total > 1 ? n_total : 1)) return AK_ERR_INVALID_SECTION_COUNT;
+    if (nl + nh != n_total) return AK_ERR_VALUE;
+    if (dtype == AK_F32)
+        return run_plan<float>(lprefix, nl, hprefix, nh, h_w, n_total, s, avg, lcounts, hcounts,
+                               spills, method, ak_stream(stream));
+    if (dtype == AK_F64)
+        return run_plan<double>(lprefix, nl, hprefix, nh, h_w, n_total, s, avg, lcounts, hcounts,
+                                spills, method, ak_stream(stream));
+    return AK_ERR_VALUE;
+}
+
+int ak_partial_pary_search(const double *hay, uint64_t n, const double *q, uint64_t m,
+                           uint32_t p, int64_t *out, void *stream)
+{
+    cudaStream_t st = ak_stream(stream);
+    if (p < 3) return AK_ERR_VALUE;
+    int *flag = nullptr;
+    i64 *ab = nullptr;
+    AK_CUDA_TRY(cudaMallocAsync((void **)&flag, 64, st));
+    ab = (i64 *)((char *)flag + 16);
+    AK_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    if (n > 1) k_check_sorted<<<64, 256, 0, st>>>(hay, n, flag);
+    int f1 = 0, f2 = 0;
+    AK_CUDA_TRY(cudaMemcpyAsync(&f1, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    AK_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    if (m > 1) k_check_sorted<<<64, 256, 0, st>>>(q, m, flag);
+    AK_CUDA_TRY(cudaMemcpyAsync(&f2, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    AK_CUDA_TRY(cudaStreamSynchronize(st));
+    AK_LAUNCH_CHECK("k_check_sorted");
+    int rc = AK_OK;
+    if (f1 || f2) rc = AK_ERR_UNSORTED_INPUT;
+    else if (m > 0) {
+        k_contract<<<1, 32, 0, st>>>(hay, n, q, m, (int)p, ab);
+        k_lower_bound<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(hay, q, m, ab, out);
+        rc = ak_check_launch("k_lower_bound");
+    }
+    cudaFreeAsync(flag, st);
+    return rc;
+}
+
+int ak_pack_sections(const int64_t *l_idx, const void *l_w, uint64_t nl, const int64_t *h_idx,
+                     const void *h_w, uint64_t nh, int dtype, const int64_t *lcounts,
+                     const int64_t *hcounts, const double *spills, uint64_t s,
+                     uint64_t sec_first, uint64_t sec_last, double avg, void *rows,
+                     double *out_spills, uint32_t chunk_capacity, void *stream)
+{
+    if (sec_first < 1 || sec_last > s || sec_first > sec_last) return AK_ERR_PLAN_INCONSISTENT;
+    if (chunk_capacity == 1) return AK_ERR_VALUE;
+    if (dtype == AK_F32)
+        return run_pack<float>(l_idx, l_w, nl, h_idx, h_w, nh, lcounts, hcounts, spills, s,
+                               sec_first, sec_last, avg, rows, out_spills, chunk_capacity,
+                               ak_stream(stream));
+    if (dtype == AK_F64)
+        return run_pack<double>(l_idx, l_w, nl, h_idx, h_w, nh, lcounts, hcounts, spills, s,
+                                sec_first, sec_last, avg, rows, out_spills, chunk_capacity,
+                                ak_stream(stream));
+    return AK_ERR_VALUE;
+}
+
+}  // extern "C"

@@ -1,0 +1,243 @@
+// ak_verify.cu — device verification and layout conversion.
+//
+//   ak_validate_table    validate_table (model.py:111-144): row invariants and
+//                        per-item reconstructed mass.  Each donated row adds
+//                        avg - tw to its alias with a compensated f64 atomic:
+//                        the rounding error of every atomicAdd is recovered
+//                        exactly from the returned old value (TwoSum) and
+//                        accumulated separately, so heavy items receiving
+//                        millions of contributions are still reconstructed to
+//                        ~1 ulp.
+//   ak_frequency_counts  frequency_counts (stats.py:25-32)
+//   ak_rows_to_soa / ak_soa_to_rows / ak_count_unwritten
+#include "ak_common.cuh"
+
+namespace {
+
+template <typename RowT>
+__global__ void k_donate(const RowT *__restrict__ rows, u64 n, double avg, double row_tol,
+                         double *hi, double *lo, int *bad_rows)
+{
+    u64 stride = (u64)gridDim.x * blockDim.x;
+    int bad = 0;
+    for (u64 j = (u64)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+        RowT r = rows[j];
+        double tw = (double)r.tw;
+        u64 a = (u64)r.alias;
+        if (!isfinite(tw) || !(tw >= 0.0) || !(tw <= avg * (1.0 + row_tol)) || a < 1 || a > n) bad = 1;
+        if (a >= 1 && a <= n && a != j + 1) {
+            double c = avg - tw;
+            double old = atomicAdd(&hi[a - 1], c);
+            double s, e;
+            two_sum(old, c, s, e);
+            if (e != 0.0) atomicAdd(&lo[a - 1], e);
+        }
+    }
+    if (bad) atomicOr(bad_rows, 1);
+}
+
+template <typename RowT, typename W>
+__global__ void k_mass(const RowT *__restrict__ rows, const W *__restrict__ w, u64 n,
+                       const double *__restrict__ hi, const double *__restrict__ lo,
+                       unsigned long long *worst_bits)
+{
+    u64 stride = (u64)gridDim.x * blockDim.x;
+    double best = -1.0;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        double wi = (double)w[i];
+        // received = tw + (hi + lo), evaluated in double-double
+        dd rec = dd_add_d(dd_add_d(dd_make(hi[i]), lo[i]), (double)rows[i].tw);
+        dd diff = dd_add_d(rec, -wi);
+        double rel = fabs(diff.hi + diff.lo) / wi;
+        if (!(rel <= 1e300)) rel = 1e300;  // NaN / inf -> huge
+        best = fmax(best, rel);
+    }
+    if (best >= 0.0) atomicMax(worst_bits, (unsigned long long)__double_as_longlong(best));
+}
+
+template <typename RowT, typename W>
+__global__ void k_mass_argmax(const RowT *__restrict__ rows, const W *__restrict__ w, u64 n,
+                              const double *__restrict__ hi, const double *__restrict__ lo,
+                              const unsigned long long *worst_bits, unsigned long long *first)
+{
+    const double target = __longlong_as_double((long long)*worst_bits);
+    u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        double wi = (double)w[i];
+        dd rec = dd_add_d(dd_add_d(dd_make(hi[i]), lo[i]), (double)rows[i].tw);
+        dd diff = dd_add_d(rec, -wi);
+        double rel = fabs(diff.hi + diff.lo) / wi;
+        if (!(rel <= 1e300)) rel = 1e300;
+        if (rel == target) atomicMin(first, (unsigned long long)i);
+    }
+}
+
+__global__ void k_freq(const i64 *__restrict__ s, u64 m, u64 n, unsigned long long *counts,
+                       int *oor)
+{
+    u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+        i64 v = s[i];
+        if (v < 1 || (u64)v > n) {
+            atomicOr(oor, 1);
+            continue;
+        }
+        atomicAdd(&counts[v - 1], 1ull);
+    }
+}
+
+template <typename RowT>
+__global__ void k_to_soa(const RowT *__restrict__ rows, u64 n, double *tw, i64 *alias)
+{
+    u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        RowT r = rows[i];
+        tw[i] = (double)r.tw;
+        alias[i] = (i64)r.alias;
+    }
+}
+
+template <typename RowT>
+__global__ void k_from_soa(const double *tw, const i64 *alias, u64 n, RowT *rows)
+{
+    typedef decltype(RowT::tw) TwT;
+    typedef decltype(RowT::alias) AT;
+    u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        RowT r;
+        r.tw = (TwT)tw[i];
+        r.alias = (AT)alias[i];
+        rows[i] = r;
+    }
+}
+
+template <typename RowT>
+__global__ void k_unwritten(const RowT *__restrict__ rows, u64 n, unsigned long long *cnt)
+{
+    u64 stride = (u64)gridDim.x * blockDim.x;
+    unsigned long long c = 0;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        c += rows[i].alias == 0;
+    if (c) atomicAdd(cnt, c);
+}
+
+int grid_of(u64 n)
+{
+    u64 g = (n + 255) / 256;
+    u64 cap = (u64)ak_num_sms() * 8;
+    return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+template <typename RowT, typename W>
+int run_validate(const void *rows, u64 n, const void *w, double avg, double row_tol, int *rows_ok,
+                 double *worst_rel, int64_t *worst_item, void *ws, cudaStream_t st)
+{
+    double *hi = (double *)ws;
+    double *lo = hi + n;
+    unsigned long long *misc = (unsigned long long *)(lo + n);  // [0] worst, [1] first
+    int *bad = (int *)(misc + 2);
+    AK_CUDA_TRY(cudaMemsetAsync(hi, 0, 2 * n * sizeof(double), st));
+    AK_CUDA_TRY(cudaMemsetAsync(misc, 0, 2 * sizeof(unsigned long long) + 16, st));
+    AK_CUDA_TRY(cudaMemsetAsync(misc + 1, 0xff, sizeof(unsigned long long), st));
+    k_donate<RowT><<<grid_of(n), 256, 0, st>>>((const RowT *)rows, n, avg, row_tol, hi, lo, bad);
+    k_mass<RowT, W><<<grid_of(n), 256, 0, st>>>((const RowT *)rows, (const W *)w, n, hi, lo, misc);
+    k_mass_argmax<RowT, W><<<grid_of(n), 256, 0, st>>>((const RowT *)rows, (const W *)w, n, hi, lo,
+                                                      misc, misc + 1);
+    AK_LAUNCH_CHECK("k_validate");
+    unsigned long long hm[2];
+    int b = 0;
+    AK_CUDA_TRY(cudaMemcpyAsync(hm, misc, sizeof(hm), cudaMemcpyDeviceToHost, st));
+    AK_CUDA_TRY(cudaMemcpyAsync(&b, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    AK_CUDA_TRY(cudaStreamSynchronize(st));
+    *rows_ok = !b;
+    *worst_rel = __builtin_bit_cast(double, hm[0]);
+    *worst_item = (int64_t)hm[1] + 1;
+    return AK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t ak_validate_workspace_bytes(uint64_t n) { return 2 * n * sizeof(double) + 256; }
+
+int ak_validate_table(const void *rows, int dtype, uint64_t n, const void *w, int w_dtype,
+                      double avg, double row_tol, int *rows_ok, double *worst_rel,
+                      int64_t *worst_item, void *ws, size_t ws_bytes, void *stream)
+{
+    if (n == 0) return AK_ERR_EMPTY_INPUT;
+    if (ws_bytes < ak_validate_workspace_bytes(n)) return AK_ERR_WORKSPACE;
+    cudaStream_t st = ak_stream(stream);
+    if (dtype == AK_F32 && w_dtype == AK_F32)
+        return run_validate<RowF32, float>(rows, n, w, avg, row_tol, rows_ok, worst_rel, worst_item, ws, st);
+    if (dtype == AK_F32 && w_dtype == AK_F64)
+        return run_validate<RowF32, double>(rows, n, w, avg, row_tol, rows_ok, worst_rel, worst_item, ws, st);
+    if (dtype == AK_F64 && w_dtype == AK_F32)
+        return run_validate<RowF64, float>(rows, n, w, avg, row_tol, rows_ok, worst_rel, worst_item, ws, st);
+    if (dtype == AK_F64 && w_dtype == AK_F64)
+        return run_validate<RowF64, double>(rows, n, w, avg, row_tol, rows_ok, worst_rel, worst_item, ws, st);
+    return AK_ERR_VALUE;
+}
+
+int ak_frequency_counts(const int64_t *samples, uint64_t m, uint64_t n, int64_t *counts,
+                        void *stream)
+{
+    cudaStream_t st = ak_stream(stream);
+    if (n < 1) return AK_ERR_VALUE;
+    int *oor = nullptr;
+    AK_CUDA_TRY(cudaMallocAsync((void **)&oor, 16, st));
+    AK_CUDA_TRY(cudaMemsetAsync(oor, 0, 16, st));
+    AK_CUDA_TRY(cudaMemsetAsync(counts, 0, n * sizeof(int64_t), st));
+    if (m) k_freq<<<grid_of(m), 256, 0, st>>>(samples, m, n, (unsigned long long *)counts, oor);
+    int f = 0;
+    AK_CUDA_TRY(cudaMemcpyAsync(&f, oor, sizeof(int), cudaMemcpyDeviceToHost, st));
+    AK_CUDA_TRY(cudaStreamSynchronize(st));
+    cudaFreeAsync(oor, st);
+    AK_LAUNCH_CHECK("k_freq");
+    return f ? AK_ERR_INDEX_OUT_OF_RANGE : AK_OK;
+}
+
+int ak_rows_to_soa(const void *rows, int dtype, uint64_t n, double *tw, int64_t *alias,
+                   void *stream)
+{
+    if (n == 0) return AK_OK;
+    cudaStream_t st = ak_stream(stream);
+    if (dtype == AK_F32) k_to_soa<RowF32><<<grid_of(n), 256, 0, st>>>((const RowF32 *)rows, n, tw, alias);
+    else if (dtype == AK_F64) k_to_soa<RowF64><<<grid_of(n), 256, 0, st>>>((const RowF64 *)rows, n, tw, alias);
+    else return AK_ERR_VALUE;
+    AK_LAUNCH_CHECK("k_to_soa");
+    return AK_OK;
+}
+
+int ak_soa_to_rows(const double *tw, const int64_t *alias, uint64_t n, int dtype, void *rows,
+                   void *stream)
+{
+    if (n == 0) return AK_OK;
+    cudaStream_t st = ak_stream(stream);
+    if (dtype == AK_F32) k_from_soa<RowF32><<<grid_of(n), 256, 0, st>>>(tw, alias, n, (RowF32 *)rows);
+    else if (dtype == AK_F64) k_from_soa<RowF64><<<grid_of(n), 256, 0, st>>>(tw, alias, n, (RowF64 *)rows);
+    else return AK_ERR_VALUE;
+    AK_LAUNCH_CHECK("k_from_soa");
+    return AK_OK;
+}
+
+int ak_count_unwritten(const void *rows, int dtype, uint64_t n, uint64_t *unwritten, void *stream)
+{
+    cudaStream_t st = ak_stream(stream);
+    unsigned long long *c = nullptr;
+    AK_CUDA_TRY(cudaMallocAsync((void **)&c, 16, st));
+    AK_CUDA_TRY(cudaMemsetAsync(c, 0, 16, st));
+    if (n) {
+        if (dtype == AK_F32) k_unwritten<RowF32><<<grid_of(n), 256, 0, st>>>((const RowF32 *)rows, n, c);
+        else k_unwritten<RowF64><<<grid_of(n), 256, 0, st>>>((const RowF64 *)rows, n, c);
+    }
+    unsigned long long h = 0;
+    AK_CUDA_TRY(cudaMemcpyAsync(&h, c, sizeof(h), cudaMemcpyDeviceToHost, st));
+    AK_CUDA_TRY(cudaStreamSynchronize(st));
+    cudaFreeAsync(c, st);
+    AK_LAUNCH_CHECK("k_unwritten");
+    *unwritten = h;
+    return AK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,172 @@
+"""Drawing weighted samples (mirror of aliaskit/sample.py) on the device.
+
+``sample_batch``: one Philox counter per draw and the bucket rule over the
+whole table (ak_sample_naive, sample.py:73-149).  ``sectioned_sample``:
+binomial section counts from the communication-free recursion (host C++,
+bit-exact with sample.py:152-240), then one CTA per section draws from the
+section's rows staged in shared memory (ak_sample_sectioned,
+sample.py:243-267).  With ``rng="reference"`` (default) both are
+bit-identical to the reference for the same RngStream; ``rng="philox4x32"``
+is the GPU-native stream (two draws per Philox4x32-10 call), checked by
+chi-square goodness of fit.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import InvalidSectionSize
+from .model import AliasTable, rng_uniform
+from .rng import MASK64, RngStream
+
+__all__ = [
+    "InvalidSectionSize",
+    "SectionAssignment",
+    "sample_one",
+    "sample_batch",
+    "sample_from_uniforms",
+    "assign_sections",
+    "assign_subtree",
+    "sectioned_sample",
+    "sectioned_sample_into",
+]
+
+
+@dataclass
+class SectionAssignment:
+    """Per-section sample counts plus their key material (sample.py:44-56)."""
+
+    section_size: int
+    counts: np.ndarray
+    total: int
+    seed: int
+    stream: int
+
+    @property
+    def n_sections(self) -> int:
+        return int(self.counts.size)
+
+
+def _rng_code(rng: str) -> int:
+    try:
+        return _lib.RNG_MODES[rng]
+    except KeyError:
+        raise ValueError(f"unknown rng mode {rng!r}: expected one of {sorted(_lib.RNG_MODES)}")
+
+
+def sample_one(t: AliasTable, r: RngStream) -> int:
+    """One weighted draw (host uniform, one row read); advances r by one."""
+    u = rng_uniform(r)
+    x = u * t.n
+    k0 = int(x)
+    if k0 >= t.n:
+        k0 = t.n - 1
+    tw = float(t.tw[k0].item())
+    if (x - k0) * t.average < tw:
+        return k0 + 1
+    return int(t.alias[k0].item())
+
+
+def sample_batch(t: AliasTable, m: int, r: RngStream, workers: int = 1, rng: str = "reference",
+                 out: torch.Tensor | None = None) -> torch.Tensor:
+    """m independent draws (1-based item ids, device int64); advances r by m.
+
+    ``workers`` is accepted for API parity; the output never depends on it
+    (sample.py:131-147), as on the reference.
+    """
+    if m < 0:
+        raise ValueError("sample count must be non-negative")
+    dev = t.rows.device
+    if out is None:
+        out = torch.empty(m, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().ak_sample_naive(
+            _lib.ptr(t.rows), t.dtype_code, t.n, t.average, 0, t.n, r.seed, r.stream,
+            r.counter & MASK64, m, _lib.ptr(out), _rng_code(rng), _lib.stream_ptr(dev)),
+            "sample_batch")
+    r.counter += m
+    return out
+
+
+def sample_from_uniforms(t: AliasTable, u, lo: int = 0, span: int | None = None) -> torch.Tensor:
+    """The bucket rule on explicit uniforms (tests/test_sample.py:20-25)."""
+    dev = t.rows.device
+    uu = torch.as_tensor(u, dtype=torch.float64, device=dev).contiguous()
+    span = t.n if span is None else span
+    out = torch.empty(uu.numel(), dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().ak_sample_from_uniforms(
+            _lib.ptr(t.rows), t.dtype_code, t.n, t.average, lo, span, _lib.ptr(uu), uu.numel(),
+            _lib.ptr(out), _lib.stream_ptr(dev)), "sample_from_uniforms")
+    return out
+
+
+def _num_sections(n_rows: int, S: int) -> tuple[int, int]:
+    S = min(S, n_rows)
+    return S, -(-n_rows // S)
+
+
+def assign_subtree(n_rows: int, S: int, seed: int, a: int, b: int, m: int,
+                   stream: int = 0) -> np.ndarray:
+    """Counts for sections [a, b) given that subtree's total m
+    (sample.py:222-240); bit-exact host C++ (ak_assign_subtree)."""
+    if S < 1:
+        raise InvalidSectionSize(f"section size {S} must be at least 1")
+    S, ns = _num_sections(n_rows, S)
+    if not 0 <= a < b <= ns:
+        raise ValueError(f"subtree [{a}, {b}) outside 0..{ns}")
+    counts = np.zeros(b - a, dtype=np.int64)
+    _lib.check(_lib.lib().ak_assign_subtree(n_rows, S, seed & MASK64, stream & MASK64, a, b, m,
+                                            counts.ctypes.data), "assign_subtree")
+    return counts
+
+
+def assign_sections(n_rows: int, S: int, M: int, seed: int, stream: int = 0) -> SectionAssignment:
+    """Deterministic per-section sample counts summing exactly to M
+    (sample.py:203-219)."""
+    if n_rows < 1:
+        raise ValueError("n_rows must be positive")
+    if S < 1:
+        raise InvalidSectionSize(f"section size {S} must be at least 1")
+    if M < 0:
+        raise ValueError("sample count must be non-negative")
+    S_eff, ns = _num_sections(n_rows, S)
+    counts = assign_subtree(n_rows, S_eff, seed, 0, ns, M, stream)
+    return SectionAssignment(section_size=S_eff, counts=counts, total=M, seed=seed, stream=stream)
+
+
+def sectioned_sample_into(t: AliasTable, S_eff: int, counts_d: torch.Tensor,
+                          offsets_d: torch.Tensor, first: int, count: int, r: RngStream,
+                          out: torch.Tensor, out_base: int, rng: str = "reference") -> None:
+    """Draw sections [first, first+count) into out[offsets - out_base ...]
+    without touching r (the building block of sectioned_sample and of the
+    multi-GPU / multi-pass drivers)."""
+    dev = t.rows.device
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().ak_sample_sectioned(
+            _lib.ptr(t.rows), t.dtype_code, t.n, t.average, S_eff, _lib.ptr(counts_d),
+            _lib.ptr(offsets_d), first, count, r.seed, r.stream, r.counter & MASK64,
+            _lib.ptr(out), out_base, _rng_code(rng), _lib.stream_ptr(dev)), "sectioned_sample")
+
+
+def sectioned_sample(t: AliasTable, S: int, M: int, r: RngStream, rng: str = "reference",
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+    """M draws confined section by section to contiguous row ranges
+    (sample.py:243-267); section-major output; advances r by M."""
+    if M < 0:
+        raise ValueError("sample count must be non-negative")
+    asg = assign_sections(t.n, S, M, r.seed, r.stream)
+    dev = t.rows.device
+    if out is None:
+        out = torch.empty(M, dtype=torch.int64, device=dev)
+    if M:
+        counts = torch.from_numpy(asg.counts).to(dev)
+        offsets = torch.from_numpy(np.concatenate([[0], np.cumsum(asg.counts)[:-1]])).to(dev)
+        sectioned_sample_into(t, asg.section_size, counts, offsets, 0, asg.n_sections, r, out, 0,
+                              rng)
+    r.counter += M
+    return out

@@ -1,0 +1,292 @@
+"""GPU parity: RNG, make_weight_set, validate_table, partition, split plan,
+pack sweep, partial p-ary search — each against the golden fixtures (made
+from the reference) and the oracle, through the C-ABI library."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2106_12270_b200 as ak
+from paper_2106_12270_b200 import _lib
+from paper_2106_12270_b200.pack import pack_all
+from conftest import random_weights
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+# ---- rng --------------------------------------------------------------------
+
+def test_philox_kats_on_device(hand):
+    kats = hand["philox2x64_10_kat"]
+    ctr = torch.tensor([int(k["ctr"][0], 16) for k in kats], dtype=torch.uint64, device=DEV)
+    strm = torch.tensor([int(k["ctr"][1], 16) for k in kats], dtype=torch.uint64, device=DEV)
+    key = torch.tensor([int(k["key"], 16) for k in kats], dtype=torch.uint64, device=DEV)
+    w0 = torch.empty(3, dtype=torch.uint64, device=DEV)
+    w1 = torch.empty(3, dtype=torch.uint64, device=DEV)
+    _lib.check(_lib.lib().ak_philox2x64(ctr.data_ptr(), strm.data_ptr(), key.data_ptr(), 3,
+                                        w0.data_ptr(), w1.data_ptr(), _lib.stream_ptr()))
+    got0 = [int(x) & (2**64 - 1) for x in w0.cpu().view(torch.int64).tolist()]
+    got1 = [int(x) & (2**64 - 1) for x in w1.cpu().view(torch.int64).tolist()]
+    assert got0 == [int(k["w0"], 16) for k in kats]
+    assert got1 == [int(x, 16) for x in hand["philox2x64_10_kat_w1_random123"]]
+
+
+def test_uniform_block_golden_and_wrap(golden):
+    r = ak.RngStream(20260815)
+    assert np.array_equal(ak.uniform_block(r, 1000).cpu().numpy(), golden["ub_a"])
+    assert r.counter == 1000
+    r = ak.RngStream(7, 3, (1 << 64) - 5)
+    assert np.array_equal(ak.uniform_block(r, 16).cpu().numpy(), golden["ub_b"])
+
+
+def test_uniform_block_resume(rng):
+    r = ak.RngStream(seed=7, stream=3, counter=50)
+    a = ak.uniform_block(r, 10)
+    b = ak.uniform_block(r, 10)
+    both = ak.uniform_block(ak.RngStream(7, 3, 50), 20)
+    assert torch.equal(torch.cat([a, b]), both)
+    big = ak.uniform_block(ak.RngStream(99, 1, 123), 1_000_003).cpu().numpy()
+    assert np.array_equal(big, O.uniform_block(99, 1, 123, 1_000_003))
+
+
+# ---- make_weight_set / validate_table ---------------------------------------
+
+def test_weight_set_totals_bit_identical_to_np_sum(golden, rng):
+    for ci in range(len(golden["sizes"])):
+        w = golden[f"c{ci}_weights"]
+        assert ak.make_weight_set(w).total == float(golden[f"c{ci}_total"][0])
+    for n in (1, 7, 8, 9, 127, 128, 129, 2049, 100_003, 3_000_001):
+        w = random_weights(rng, n, n % 5)
+        assert ak.make_weight_set(w).total == float(np.sum(w))
+        w32 = w.astype(np.float32)
+        ws = ak.make_weight_set(torch.from_numpy(w32).to(DEV))
+        assert ws.dtype == torch.float32
+        assert ws.total == float(np.sum(w32.astype(np.float64)))
+
+
+@pytest.mark.parametrize("bad,idx", [([1.0, 0.0, 2.0], 2), ([1.0, -3.0], 2),
+                                     ([float("nan"), 1.0], 1), ([1.0, float("inf")], 2)])
+def test_invalid_weight_reports_1based_index(bad, idx):
+    with pytest.raises(ak.InvalidWeight) as e:
+        ak.make_weight_set(bad)
+    assert e.value.index == idx
+
+
+def test_invalid_weight_first_bad_wins_at_scale():
+    w = torch.rand(5_000_000, dtype=torch.float64, device=DEV) + 0.5
+    w[4_000_001] = -1.0
+    w[3_999_999] = float("nan")
+    with pytest.raises(ak.InvalidWeight) as e:
+        ak.make_weight_set(w)
+    assert e.value.index == 4_000_000
+
+
+def test_empty_and_shape():
+    with pytest.raises(ak.EmptyInput):
+        ak.make_weight_set([])
+    with pytest.raises(ValueError):
+        ak.make_weight_set(np.ones((2, 2)))
+
+
+def test_validate_table_matches_oracle(golden, rng):
+    for ci in range(len(golden["sizes"])):
+        w = golden[f"c{ci}_weights"]
+        ws = ak.make_weight_set(w)
+        t = ak.AliasTable.from_numpy(golden[f"c{ci}_vose_tw"], golden[f"c{ci}_vose_alias"], ws.n, ws.total)
+        rep = ak.validate_table(t, ws)
+        g = golden[f"c{ci}_vose_valid"]
+        assert rep.ok == bool(g[2])
+        assert abs(rep.worst_rel_error - g[0]) <= 1e-15 + 1e-6 * g[0]
+    ws = ak.make_weight_set([3.0, 1.0, 2.0, 2.0])
+    bad = ak.AliasTable.from_numpy([2.0, 2.0, 2.0, 2.0], [1, 1, 3, 4], 4, 8.0)
+    rep = ak.validate_table(bad, ws)
+    assert not rep.ok and rep.worst_item in (1, 2)
+    over = ak.AliasTable.from_numpy([1.5, 0.5], [1, 1], 2, 2.0)
+    assert not ak.validate_table(over, ak.make_weight_set([1.0, 1.0])).ok
+    with pytest.raises(ak.SizeMismatch):
+        ak.validate_table(ak.AliasTable.from_numpy(np.ones(3), np.ones(3), 3, 3.0),
+                          ak.make_weight_set([1.0, 1.0]))
+
+
+# ---- partition / plan / pack -------------------------------------------------
+
+def _ref_partition(golden, ci):
+    k = f"c{ci}_"
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    w = golden[k + "weights"]
+    tot = float(golden[k + "total"][0])
+    return ak.LightHeavyPartition(t(golden[k + "l_index"]), t(golden[k + "l_weight"]),
+                                  t(golden[k + "h_index"]), t(golden[k + "h_weight"]),
+                                  t(golden[k + "lprefix"]), t(golden[k + "hprefix"]), tot / w.size)
+
+
+def test_partition_matches_reference(golden, hand):
+    p = ak.partition_items(ak.make_weight_set(hand["table4"]["w"]))
+    assert p.l == [tuple(x) for x in hand["partition4"]["l"]]
+    assert p.h == [tuple(x) for x in hand["partition4"]["h"]]
+    assert p.lprefix.tolist() == hand["partition4"]["lprefix"]
+    for ci in range(len(golden["sizes"])):
+        k = f"c{ci}_"
+        p = ak.partition_items(ak.make_weight_set(golden[k + "weights"]))
+        for f in ("l_index", "l_weight", "h_index", "h_weight"):
+            assert np.array_equal(getattr(p, f).cpu().numpy(), golden[k + f]), f
+        for f in ("lprefix", "hprefix"):
+            got, want = getattr(p, f).cpu().numpy(), golden[k + f]
+            ulp = np.spacing(np.maximum(np.abs(want), 1e-300))
+            assert np.all(np.abs(got - want) <= 2 * ulp), f  # dd-exact vs Neumaier
+
+
+def test_prefix_sums_recover_increments(rng):
+    ws = ak.make_weight_set(rng.pareto(1.1, 30000) + 1e-6)
+    p = ak.partition_items(ws)
+    for pre, w in ((p.lprefix, p.l_weight), (p.hprefix, p.h_weight)):
+        pre, w = pre.cpu().numpy(), w.cpu().numpy()
+        d = np.abs(np.diff(pre) - w)
+        ulp = np.spacing(np.maximum(np.abs(pre[1:]), np.abs(pre[:-1])))
+        assert np.all(d <= 4 * ulp)
+
+
+@pytest.mark.parametrize("method", ["binary", "batched"])
+def test_split_plan_bit_identical_on_reference_partition(golden, method):
+    for ci in range(len(golden["sizes"])):
+        p = _ref_partition(golden, ci)
+        for s in (1, 2, 7, 64):
+            if s > p.n:
+                continue
+            plan = ak.compute_split_plan(p, s, method=method)
+            k = f"c{ci}_plan{s}_"
+            assert np.array_equal(plan.lcounts.cpu().numpy(), golden[k + "l"])
+            assert np.array_equal(plan.hcounts.cpu().numpy(), golden[k + "h"])
+            assert np.array_equal(plan.spills.cpu().numpy(), golden[k + "sp"])
+
+
+@pytest.mark.parametrize("method", ["binary", "batched"])
+def test_split_plan_many_boundaries_vs_oracle(rng, method):
+    for trial in range(12):
+        n = int(rng.integers(2, 300_000))
+        w = random_weights(rng, n, trial % 5)
+        _, tot = O.make_weight_set(w)
+        po = O.partition_items(w, tot)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+        p = ak.LightHeavyPartition(t(po["l_index"]), t(po["l_weight"]), t(po["h_index"]),
+                                   t(po["h_weight"]), t(po["lprefix"]), t(po["hprefix"]), po["avg"])
+        for s in (3, 1000, n // 7 + 1, n):
+            lc, hc, sp = O.compute_split_plan(po["lprefix"], po["hprefix"], po["h_weight"], n, s, po["avg"])
+            plan = ak.compute_split_plan(p, s, method=method)
+            assert np.array_equal(plan.lcounts.cpu().numpy(), lc)
+            assert np.array_equal(plan.hcounts.cpu().numpy(), hc)
+            assert np.array_equal(plan.spills.cpu().numpy(), sp)
+
+
+def test_plan_hand_and_validation(hand):
+    p = ak.partition_items(ak.make_weight_set(hand["table4"]["w"]))
+    assert [list(b) for b in ak.compute_split_plan(p, 2).boundaries] == hand["plan4_s2"]
+    assert ak.compute_split_plan(p, 1).boundaries == [(0, 0, 0.0), (3, 1, 0.0)]
+    p12 = ak.partition_items(ak.make_weight_set([2.0] * 12))
+    plan = ak.compute_split_plan(p12, 4)
+    assert plan.lcounts.tolist() == hand["plan_equal12_s4_l"] and plan.hcounts.tolist() == [0] * 5
+    with pytest.raises(ak.InvalidSectionCount):
+        ak.compute_split_plan(p, 0)
+    with pytest.raises(ak.InvalidSectionCount):
+        ak.compute_split_plan(p, 5)
+    assert ak.binary_search_boundary(p, 0, 0.0) == (0, 0, 0.0)
+
+
+@pytest.mark.parametrize("cap", [0, 2, 3, 64, 10**6])
+def test_pack_sections_bit_identical(golden, cap):
+    """The reference's sweep on its own partition and plan -> its psa table."""
+    for ci in range(len(golden["sizes"])):
+        p = _ref_partition(golden, ci)
+        n = p.n
+        tot = float(golden[f"c{ci}_total"][0])
+        for s in (1, 2, 7, 64):
+            if s > n:
+                continue
+            plan = ak.compute_split_plan(p, s, method="binary")
+            out = ak.AliasTable.blank(n, tot)
+            if cap == 0:
+                for i in range(1, s + 1):
+                    ak.pack_section(p, plan, i, out)
+            else:
+                pack_all(p, plan, out, cap)
+            tw, al = out.to_numpy()
+            assert np.array_equal(tw, golden[f"c{ci}_psa{s}_tw"])
+            assert np.array_equal(al, golden[f"c{ci}_psa{s}_alias"])
+
+
+def test_pack_section_spills_and_ownership(rng):
+    for trial in range(6):
+        n = int(rng.integers(4, 800))
+        ws = ak.make_weight_set(random_weights(rng, n, trial % 3))
+        p = ak.partition_items(ws)
+        s = min(5, n)
+        plan = ak.compute_split_plan(p, s)
+        out = ak.AliasTable.blank(n, ws.total)
+        for i in range(1, s + 1):
+            before = out.tw.clone()
+            got = ak.pack_section(p, plan, i, out)
+            touched = torch.nonzero(out.tw != before).flatten().cpu().numpy()
+            la, lb = plan.lcounts[i - 1].item(), plan.lcounts[i].item()
+            ha, hb = plan.hcounts[i - 1].item(), plan.hcounts[i].item()
+            owned = np.concatenate([p.l_index[la:lb].cpu().numpy(), p.h_index[ha:hb].cpu().numpy()]) - 1
+            assert np.array_equal(np.sort(owned), touched)
+            if i < s and plan.hcounts[i].item() < p.h_index.numel():
+                assert got == pytest.approx(plan.spills[i].item(), abs=1e-9 * p.avg)
+        assert ak.validate_table(out, ws).ok
+
+
+def test_plan_tampering_rejected():
+    ws = ak.make_weight_set([3.0, 1.0, 2.0, 2.0, 5.0, 1.0])
+    p = ak.partition_items(ws)
+    plan = ak.compute_split_plan(p, 2)
+    out = ak.AliasTable.blank(ws.n, ws.total)
+    bad = ak.SplitPlan(2, plan.lcounts.clone(), plan.hcounts.clone(), plan.spills.clone())
+    bad.lcounts[-1] += 1
+    with pytest.raises(ak.PlanInconsistent):
+        ak.pack_section(p, bad, 1, out)
+    bad2 = ak.SplitPlan(2, plan.lcounts.clone(), plan.hcounts.clone(), plan.spills.clone())
+    bad2.lcounts[1] = bad2.lcounts[2] + 1
+    with pytest.raises(ak.PlanInconsistent):
+        ak.pack_section(p, bad2, 1, out)
+    with pytest.raises(ak.PlanInconsistent):
+        ak.pack_section(p, plan, 0, out)
+    with pytest.raises(ak.PlanInconsistent):
+        ak.pack_section(p, plan, 3, out)
+    with pytest.raises(ValueError):
+        ak.chunked_pack_section(p, plan, 1, 1, out)
+
+
+# ---- partial p-ary search ----------------------------------------------------
+
+def test_pary_golden_and_hand(golden, hand):
+    for p in (3, 8, 32):
+        got = ak.partial_pary_search(golden["pary_hay"], golden["pary_q"], p=p).cpu().numpy()
+        assert np.array_equal(got, golden[f"pary_{p}"])
+    h = hand["pary_hand"]
+    assert ak.partial_pary_search(h["hay"], h["q"], p=h["p"]).tolist() == h["out"]
+    t = hand["pary_ties"]
+    assert ak.partial_pary_search(t["hay"], t["q"], p=3).tolist() == t["out"]
+    assert ak.partial_pary_search([1.0, 2.0], [], p=8).tolist() == []
+    assert ak.partial_pary_search([], [1.0, 2.0], p=3).tolist() == [0, 0]
+    with pytest.raises(ak.UnsortedInput):
+        ak.partial_pary_search([3.0, 1.0], [1.0])
+    with pytest.raises(ak.UnsortedInput):
+        ak.partial_pary_search([1.0, 3.0], [2.0, 1.0])
+    with pytest.raises(ValueError):
+        ak.partial_pary_search([1.0, 3.0], [1.0], p=2)
+
+
+def test_pary_equals_searchsorted(rng):
+    for i in range(300):
+        n = int(rng.integers(0, 100_000))
+        if i % 2:
+            hay = np.sort(rng.normal(0, 10, n))
+            q = np.sort(rng.normal(0, 12, int(rng.integers(0, 513))))
+        else:  # long tied runs
+            hay = np.sort(rng.integers(0, max(n // 4, 1), n)).astype(np.float64)
+            q = np.sort(rng.integers(-2, max(n // 4, 1) + 2, int(rng.integers(0, 513)))).astype(np.float64)
+        ref = np.searchsorted(hay, q, side="left")
+        for p in (3, 8, 32, 100):
+            assert np.array_equal(ak.partial_pary_search(hay, q, p=p).cpu().numpy(), ref)

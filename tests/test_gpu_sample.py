@@ -1,0 +1,162 @@
+"""GPU parity of both samplers: bit-exact against the reference for the same
+RngStream (golden fixtures + oracle), f32 tables bit-exact against the rule on
+the upcast table, and chi-square goodness of fit for the GPU-native RNG."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2106_12270_b200 as ak
+from paper_2106_12270_b200 import distributed as D
+from conftest import random_weights
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def table_from_golden(golden, ci, dtype=torch.float64):
+    k = f"c{ci}_"
+    n = golden[k + "weights"].size
+    return ak.AliasTable.from_numpy(golden[k + "vose_tw"], golden[k + "vose_alias"], n,
+                                    float(golden[k + "total"][0]), dtype=dtype)
+
+
+def test_rule_hand_values(hand):
+    t = ak.vose_construct(ak.make_weight_set(hand["table4"]["w"]))
+    for u, want in hand["rule4"]:
+        assert ak.sample_from_uniforms(t, [u]).item() == want
+
+
+def test_golden_samplers(golden):
+    for ci in range(len(golden["sizes"])):
+        t = table_from_golden(golden, ci)
+        seed = int(golden[f"c{ci}_seed"][0])
+        r = ak.RngStream(seed, 3, 11)
+        assert np.array_equal(ak.sample_batch(t, 2000, r).cpu().numpy(), golden[f"c{ci}_naive"])
+        assert r.counter == 2011
+        r = ak.RngStream(seed, 5, 7)
+        assert np.array_equal(ak.sectioned_sample(t, 16, 3000, r).cpu().numpy(),
+                              golden[f"c{ci}_sectioned16"])
+        assert r.counter == 3007
+
+
+def test_batch_is_sequence_of_single_draws():
+    t = ak.vose_construct(ak.make_weight_set([3.0, 1.0, 2.0, 2.0]))
+    r1, r2 = ak.RngStream(42), ak.RngStream(42)
+    batch = ak.sample_batch(t, 64, r1)
+    assert batch.tolist() == [ak.sample_one(t, r2) for _ in range(64)]
+    assert r1.counter == r2.counter == 64
+
+
+def test_empty_and_args():
+    t = ak.vose_construct(ak.make_weight_set([3.0, 1.0]))
+    r = ak.RngStream(1, 1)
+    assert ak.sample_batch(t, 0, r).numel() == 0 and r.counter == 0
+    assert ak.sectioned_sample(t, 2, 0, r).numel() == 0 and r.counter == 0
+    with pytest.raises(ValueError):
+        ak.sample_batch(t, -1, r)
+    with pytest.raises(ak.InvalidSectionSize):
+        ak.sectioned_sample(t, 0, 5, r)
+    with pytest.raises(ValueError):
+        ak.sample_batch(t, 5, r, rng="mt19937")
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_random_tables_bit_exact(rng, dtype):
+    for trial in range(16):
+        n = int(np.exp(rng.uniform(0, np.log(300_000)))) + 1
+        w = random_weights(rng, n, trial % 5)
+        if dtype == torch.float32:
+            w = w.astype(np.float32).astype(np.float64)
+        _, tot = O.make_weight_set(w)
+        ref = O.vose_construct(w, tot)
+        t = ak.AliasTable.from_numpy(ref.tw, ref.alias, n, tot, dtype=dtype)
+        tw, al = t.to_numpy()  # the device table as the reference would see it
+        rt = O.Table(tw, al, n, tot)
+        seed = int(rng.integers(2**63))
+        ctr = int(rng.integers(2**64)) if trial % 4 == 0 else int(rng.integers(1000))
+        got = ak.sample_batch(t, 50_000, ak.RngStream(seed, 3, ctr)).cpu().numpy()
+        assert np.array_equal(got, O.sample_batch(rt, 50_000, seed, 3, ctr))
+        for S in (1, 7, 64, 1000, 1 << 13, 1 << 14, 10**9):
+            got = ak.sectioned_sample(t, S, 40_000, ak.RngStream(seed, 9, ctr)).cpu().numpy()
+            assert np.array_equal(got, O.sectioned_sample(rt, S, 40_000, seed, 9, ctr)), S
+        u = O.uniform_block(seed, 4, 0, 10_000)
+        assert np.array_equal(ak.sample_from_uniforms(t, u).cpu().numpy(),
+                              O.rule(tw, al, tot / n, u))
+
+
+def test_sectioned_row_provenance(rng):
+    w = rng.random(300_000) + 0.01
+    ws = ak.make_weight_set(w)
+    t = ak.vose_construct(ws)
+    tw, al = t.to_numpy()
+    S, M = 1 << 14, 2_000_000
+    out = ak.sectioned_sample(t, S, M, ak.RngStream(31, 6)).cpu().numpy()
+    asg = ak.assign_sections(t.n, S, M, 31, 6)
+    off = 0
+    for j in range(asg.n_sections):
+        mj = int(asg.counts[j])
+        lo = j * asg.section_size
+        span = min(lo + asg.section_size, t.n) - lo
+        strm = O.derive_stream(31, 6, j, O.SALT_SECTION)
+        u = O.uniform_block(31, strm, 0, mj)
+        assert np.array_equal(out[off:off + mj], O.rule(tw, al, t.average, u, lo, span))
+        off += mj
+    assert off == M
+
+
+def test_shards_reassemble_single_gpu_output():
+    """Every rank's slice (naive counter blocks, sectioned section runs)
+    concatenates to the single-GPU output (the multi-GPU sharding, run here
+    rank by rank on one device)."""
+    ws = ak.gen_uniform(1_000_000, ak.RngStream(5), dtype=torch.float32)
+    t = ak.psa_construct(ws)
+    M = 3_000_001
+    full = ak.sample_batch(t, M, ak.RngStream(9, 1, 77))
+    for world in (2, 4, 8):
+        parts = [D.sample_batch_shard(t, M, ak.RngStream(9, 1, 77), g, world) for g in range(world)]
+        assert torch.equal(torch.cat(parts), full)
+    S = 1 << 14
+    fulls = ak.sectioned_sample(t, S, M, ak.RngStream(9, 2, 5))
+    for world in (2, 4, 8):
+        out = torch.full((M,), -1, dtype=torch.int64, device=DEV)
+        for g in range(world):
+            plan = D.ShardedSectioned(t, S, M, ak.RngStream(9, 2, 5), g, world)
+            piece = torch.empty(plan.draws, dtype=torch.int64, device=DEV)
+            plan.run(t, ak.RngStream(9, 2, 5), piece)
+            out[plan.out_off:plan.out_off + plan.draws] = piece
+        assert torch.equal(out, fulls)
+
+
+@pytest.mark.parametrize("rng_mode", ["reference", "philox4x32"])
+def test_chi_square_gate(rng_mode, acceptance):
+    """c5 protocol (test_acceptance.py:157-188), 20 seeds x 1e7 draws."""
+    n, M = 1000, 10**7
+    g = np.random.default_rng(0xACCE97 + 5)
+    sets = {"uniform": g.random(n) + 1e-9, "powerlaw": np.arange(1, n + 1, dtype=np.float64) ** -1.0}
+    verdicts, ok_all = [], True
+    for dist, w in sets.items():
+        ws = ak.make_weight_set(w)
+        t = ak.vose_construct(ws)
+        probs = w / w.sum()
+        for sampler, S in (("baseline", 0), ("sectioned", 64), ("sectioned", 2**14)):
+            fails = 0
+            for seed in range(20):
+                r = ak.RngStream(0xACCE97 + seed, 7 * S + (dist == "powerlaw"))
+                x = ak.sample_batch(t, M, r, rng=rng_mode) if S == 0 else \
+                    ak.sectioned_sample(t, S, M, r, rng=rng_mode)
+                _, _, passed = ak.chi_square_test(ak.frequency_counts(x, n), probs)
+                fails += not passed
+            verdicts.append(f"{dist}/{sampler}{'' if S == 0 else S}: {fails}")
+            ok_all &= fails <= 1
+    acceptance(f"{'PASS' if ok_all else 'FAIL'}  chi-square ({rng_mode}) 20 seeds x 1e7: {verdicts}")
+    assert ok_all, verdicts
+
+
+def test_frequency_counts_device():
+    c = ak.frequency_counts(torch.tensor([1, 3, 3, 2, 3], device=DEV), 4)
+    assert c.tolist() == [1, 1, 3, 0]
+    with pytest.raises(ak.IndexOutOfRange):
+        ak.frequency_counts(torch.tensor([0, 1], device=DEV), 3)
+    assert ak.frequency_counts(torch.empty(0, dtype=torch.int64, device=DEV), 2).tolist() == [0, 0]

@@ -1,0 +1,121 @@
+"""Host-side logic: multi-GPU sharding (with a world_size-2 gloo run on the
+CPU), chi-square verification harness, weight-set argument handling."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+from paper_2106_12270_b200 import distributed as D
+from paper_2106_12270_b200 import errors
+from paper_2106_12270_b200.stats import _chi2_quantile, _probit, chi_square_test
+
+
+def test_naive_shard_matches_worker_split():
+    for m in (0, 1, 5, 1000, 10**9 + 7):
+        for world in (1, 2, 3, 4, 8):
+            parts = [D.naive_shard(m, g, world) for g in range(world)]
+            assert sum(c for _, c in parts) == m
+            off = 0
+            for o, c in parts:
+                assert o == off or c == 0
+                off += c
+
+
+def test_section_shard_partitions_output(rng):
+    for _ in range(50):
+        ns = int(rng.integers(1, 5000))
+        counts = rng.integers(0, 1000, ns)
+        for world in (1, 2, 4, 8):
+            runs = [D.section_shard(counts, g, world) for g in range(world)]
+            nxt, out = 0, 0
+            for first, cnt, off, draws in runs:
+                assert first == nxt and off == out
+                assert draws == int(counts[first:first + cnt].sum())
+                nxt, out = first + cnt, out + draws
+            assert nxt == ns and out == int(counts.sum())
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(11)
+    w = rng.random(777) + 0.01
+    _, tot = O.make_weight_set(w)
+    t = O.vose_construct(w, tot)
+    # naive: each rank draws its counter block
+    m = 10_001
+    off, cnt = D.naive_shard(m, rank, world)
+    part = O.sample_batch(t, cnt, seed=42, stream=3, counter=100 + off)
+    # sectioned: each rank recomputes the counts and draws its section run
+    S, M = 16, 20_000
+    counts = O.assign_sections(t.n, S, M, 42, 5)
+    first, count, out_off, draws = D.section_shard(counts, rank, world)
+    full = O.sectioned_sample(t, S, M, 42, 5, 9)  # reference slice to compare
+    mine = full[out_off:out_off + draws]
+    parts = [None] * world
+    dist.all_gather_object(parts, (part.tolist(), out_off, mine.tolist()))
+    if rank == 0:
+        q.put(parts)
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_shards_reassemble_single_process_output():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(11)
+    w = rng.random(777) + 0.01
+    _, tot = O.make_weight_set(w)
+    t = O.vose_construct(w, tot)
+    naive = np.concatenate([np.array(p[0], dtype=np.int64) for p in parts])
+    assert np.array_equal(naive, O.sample_batch(t, 10_001, 42, 3, 100))
+    sec = np.concatenate([np.array(p[2], dtype=np.int64) for p in sorted(parts, key=lambda x: x[1])])
+    assert np.array_equal(sec, O.sectioned_sample(t, 16, 20_000, 42, 5, 9))
+
+
+def test_chi_square_harness_hand_cases():
+    stat, df, ok = chi_square_test([10.0, 0.0], [0.5, 0.5])
+    assert stat == pytest.approx(10.0) and df == 1 and ok
+    stat, df, ok = chi_square_test([1000, 0, 0, 0], [0.25] * 4)
+    assert not ok and stat == pytest.approx(3000.0)
+    stat, df, ok = chi_square_test([499, 499, 1, 1], [0.499, 0.499, 0.001, 0.001])
+    assert df == 2 and ok
+    with pytest.raises(errors.DegenerateBins):
+        chi_square_test([2, 2], [0.5, 0.5])
+    assert _probit(0.5) == 0.0
+    assert _chi2_quantile(0.999, 1) == pytest.approx(10.83, rel=0.15)
+
+
+def test_chi_square_matches_reference(reference):
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        k = int(rng.integers(2, 300))
+        probs = rng.random(k)
+        probs /= probs.sum()
+        if abs(probs.sum() - 1.0) > 1e-12:
+            continue
+        obs = rng.multinomial(int(rng.integers(10, 10**6)), probs)
+        assert chi_square_test(obs, probs) == reference.chi_square_test(obs, probs)
