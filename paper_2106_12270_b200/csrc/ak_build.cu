@@ -2,128 +2,137 @@
 //
 // Formulation.  Let d_i = avg - w_i (light deficit) and e_i = w_i - avg (heavy
 // excess).  The sequential construction (seqbuild.py:33-58) is a merge of two
-// sorted key sequences: light k has key DL(k) = sum of deficits of the lights
-// before it, heavy j has key DH(j) = sum of excess of heavies up to and
-// including it; heavy j closes before light k iff DH(j) <= DL(k).  Hence
+// sorted key sequences: light k has key DL(k) = sum of the deficits of the
+// lights before it, heavy j has key DH(j) = sum of the excess of the heavies
+// up to and including it; heavy j closes before light k iff DH(j) <= DL(k).
+// Hence
 //   light k:  alias = first heavy (in item order) with DH > DL(k), else self;
 //   heavy j:  tw = DH(j) - DL(first light with DL >= DH(j)) + avg,
 //             alias = next heavy, or itself when it is the last;
 // and the split predicate L[n-h] + H[h] <= n*avg of split.py:69-77 is exactly
 // DH(h) <= DL(n-h).  Every row follows from prefix sums, in parallel.
 //
-// Pipeline (three kernels, TILE = 2048 items):
-//  1. k_build_scan   read the weights once (128-bit loads); classify; block
-//                    scan of deficits / excess / light counts per tile; a
-//                    single-pass decoupled look-back chains the tile totals
-//                    into exclusive tile bases DLb[t], DHb[t] (double-double,
-//                    exact sums) and light counts kL[t].
-//  2. k_build_coarse merge of the two boundary sequences: for each tile the
-//                    range of heavy tiles whose keys cover its lights
-//                    (T1) and of light tiles covering its heavies (S1), and
-//                    the first heavy after it (nextH).
-//  3. k_build_pack   tile-owner pack: a CTA owns the rows of one item tile,
-//                    rescans it, resolves its lights against the covering
-//                    heavy tiles and its heavies against the covering light
-//                    tiles (usually one or two each, L2-resident because
-//                    neighbouring CTAs own them), and writes its rows once,
-//                    coalesced.  DRAM traffic ~ read w twice + write rows.
+// Keys.  Items are grouped in tiles of 2048 (8 chunks of 256, one warp each).
+// A key is (tile base, double-double) + (local offset, double): the local part
+// comes from a warp-level Kogge-Stone scan whose lane bases are clamped by a
+// running max/min into the chunk's [base, bound] so keys never decrease and
+// never pass the chunk bound; the chunk bases/bounds are a monotone scan of
+// the chunk totals done once by pass 1 and stored.  Any warp can therefore
+// rebuild the canonical keys of any chunk, bit-identically, without a block
+// barrier.  Cross-tile comparisons are exact: a local key plus the double-
+// double difference of two tile bases is formed as a normalised double-double
+// and compared with a local key.
 //
-// Keys inside a tile come from one deterministic "monotone" block scan (lane
-// and warp bases clamped by max/min so keys never decrease and never exceed
-// the tile total), so every CTA that rescans a tile sees bit-identical keys
-// and tile totals.  Cross-tile comparisons are exact: (a - b) of two local
-// f64 keys is formed as an exact double-double and compared with the
-// double-double difference of the tile bases.
+// Pipeline (three kernels):
+//  1. k_build_scan   one pass over the weights (128-bit loads): classify, chunk
+//                    scans, per-tile totals and chunk bounds; a single-pass
+//                    decoupled look-back over super-tiles (32 tiles per CTA,
+//                    so the inclusive frontier outruns DRAM) produces the
+//                    exclusive tile bases DLb[t], DHb[t] (exact double-double
+//                    sums) and light counts kL[t].
+//  2. k_build_coarse merge of the two tile-boundary sequences: for each tile
+//                    the first heavy tile covering its light keys (T1) and
+//                    the first light tile covering its heavy keys (S1), and
+//                    the first heavy after it (nextH).
+//  3. k_build_pack   warp per 256-item chunk, no block barriers: rebuild the
+//                    chunk's keys, resolve its lights against the heavy
+//                    chunks whose key ranges cover them and its heavies
+//                    against the covering light chunks (L2-resident: the
+//                    neighbouring warps own them), stage the 256 rows in
+//                    shared memory and store them once, coalesced.
+//  DRAM traffic ~ read w twice + write the rows once = the algorithmic bytes.
 #include "ak_common.cuh"
 
 namespace {
 
-constexpr int TB = 256;           // threads per CTA
-constexpr int VV = 8;             // items per thread
-constexpr int TILE = TB * VV;     // items per tile
-constexpr int NWARP = TB / 32;
+constexpr int TB = 256;            // threads per CTA
+constexpr int VV = 8;              // items per lane
+constexpr int CH = 32 * VV;        // items per chunk (one warp)
+constexpr int NW = TB / 32;        // chunks per tile
+constexpr int TILE = TB * VV;      // items per tile
+constexpr int SUPER = 32;          // tiles per pass-1 CTA (look-back granularity)
 constexpr u64 NONE64 = ~0ull;
+constexpr unsigned char NOFH = 0xFF;
 
 // ---------------------------------------------------------------------------
 // workspace layout
 // ---------------------------------------------------------------------------
 struct BuildWs {
-    u64 nt;  // tiles
+    u64 nt, nst;  // tiles, super-tiles
     unsigned int *counter;
-    u32 *status;
-    double *agg_d, *agg_e;
-    u32 *agg_n;
-    dd *inc_D, *inc_H;
-    u64 *inc_k;
-    dd *DLb, *DHb;   // [nt+1]
-    u64 *kL;         // [nt+1]
-    u64 *firstH;     // [nt]
-    u32 *T1, *S1;    // [nt+1]
-    u64 *nextH;      // [nt]
+    u32 *status;            // [nst] 0 none, 1 aggregate, 2 inclusive
+    dd *agg_D, *agg_H;      // [nst] super-tile aggregates (write once)
+    u64 *agg_k;             // [nst]
+    dd *inc_D, *inc_H;      // [nst] inclusive prefixes (write once)
+    u64 *inc_k;             // [nst]
+    dd *DLb, *DHb;          // [nt+1] exclusive tile bases
+    u64 *kL;                // [nt+1] lights before tile
+    u64 *firstH;            // [nt]
+    double *mD, *mE;        // [nt*8] chunk bounds (monotone inclusive scans)
+    unsigned char *mfh;     // [nt*8] first heavy offset in chunk, NOFH if none
+    u32 *T1, *S1;           // [nt+1]
+    u64 *nextH;             // [nt]
 };
 
 __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-__host__ __device__ inline BuildWs carve(void *ws, u64 n)
+template <typename F> inline void layout(u64 n, F &&take)
+{
+    u64 nt = (n + TILE - 1) / TILE;
+    u64 nst = (nt + SUPER - 1) / SUPER;
+    size_t sizes[19] = {256,          nst * 4,      nst * 16,       nst * 16,       nst * 8,
+                        nst * 16,     nst * 16,     nst * 8,        (nt + 1) * 16,  (nt + 1) * 16,
+                        (nt + 1) * 8, nt * 8,       nt * NW * 8,    nt * NW * 8,    nt * NW,
+                        (nt + 1) * 4, (nt + 1) * 4, nt * 8,         0};
+    for (int i = 0; i < 18; ++i) take(i, sizes[i]);
+}
+
+inline BuildWs carve(void *ws, u64 n)
 {
     BuildWs W;
-    u64 nt = (n + TILE - 1) / TILE;
-    W.nt = nt;
-    char *p = (char *)ws;
+    W.nt = (n + TILE - 1) / TILE;
+    W.nst = (W.nt + SUPER - 1) / SUPER;
+    char *base = (char *)ws;
     size_t off = 0;
-    auto take = [&](size_t bytes) {
-        char *r = p + off;
-        off += align256(bytes);
-        return r;
-    };
-    W.counter = (unsigned int *)take(256);
-    W.status = (u32 *)take(nt * 4);
-    W.agg_d = (double *)take(nt * 8);
-    W.agg_e = (double *)take(nt * 8);
-    W.agg_n = (u32 *)take(nt * 4);
-    W.inc_D = (dd *)take(nt * 16);
-    W.inc_H = (dd *)take(nt * 16);
-    W.inc_k = (u64 *)take(nt * 8);
-    W.DLb = (dd *)take((nt + 1) * 16);
-    W.DHb = (dd *)take((nt + 1) * 16);
-    W.kL = (u64 *)take((nt + 1) * 8);
-    W.firstH = (u64 *)take(nt * 8);
-    W.T1 = (u32 *)take((nt + 1) * 4);
-    W.S1 = (u32 *)take((nt + 1) * 4);
-    W.nextH = (u64 *)take(nt * 8);
+    char *p[18];
+    layout(n, [&](int i, size_t b) {
+        p[i] = base + off;
+        off += align256(b);
+    });
+    W.counter = (unsigned int *)p[0];
+    W.status = (u32 *)p[1];
+    W.agg_D = (dd *)p[2];
+    W.agg_H = (dd *)p[3];
+    W.agg_k = (u64 *)p[4];
+    W.inc_D = (dd *)p[5];
+    W.inc_H = (dd *)p[6];
+    W.inc_k = (u64 *)p[7];
+    W.DLb = (dd *)p[8];
+    W.DHb = (dd *)p[9];
+    W.kL = (u64 *)p[10];
+    W.firstH = (u64 *)p[11];
+    W.mD = (double *)p[12];
+    W.mE = (double *)p[13];
+    W.mfh = (unsigned char *)p[14];
+    W.T1 = (u32 *)p[15];
+    W.S1 = (u32 *)p[16];
+    W.nextH = (u64 *)p[17];
     return W;
 }
 
 size_t ws_bytes_for(u64 n)
 {
-    u64 nt = (n + TILE - 1) / TILE;
     size_t off = 0;
-    auto take = [&](size_t b) { off += align256(b); };
-    take(256);
-    take(nt * 4);
-    take(nt * 8);
-    take(nt * 8);
-    take(nt * 4);
-    take(nt * 16);
-    take(nt * 16);
-    take(nt * 8);
-    take((nt + 1) * 16);
-    take((nt + 1) * 16);
-    take((nt + 1) * 8);
-    take(nt * 8);
-    take((nt + 1) * 4);
-    take((nt + 1) * 4);
-    take(nt * 8);
+    layout(n, [&](int, size_t b) { off += align256(b); });
     return off + 256;
 }
 
 // ---------------------------------------------------------------------------
-// the monotone tile scan
+// loads and the canonical warp scan
 // ---------------------------------------------------------------------------
 template <typename T>
-__device__ __forceinline__ void load_items(const T *__restrict__ w, u64 n, u64 base, double v[VV])
+__device__ __forceinline__ void load8(const T *__restrict__ w, u64 n, u64 i0, double v[VV])
 {
-    const u64 i0 = base + (u64)threadIdx.x * VV;
     if (i0 + VV <= n) {
         if (sizeof(T) == 4) {
             const float4 *p = reinterpret_cast<const float4 *>(w + i0);
@@ -141,25 +150,11 @@ __device__ __forceinline__ void load_items(const T *__restrict__ w, u64 n, u64 b
         }
     } else {
 #pragma unroll
-        for (int k = 0; k < VV; ++k) v[k] = (i0 + k < n) ? (double)w[i0 + k] : -1.0;  // -1: absent
+        for (int k = 0; k < VV; ++k) v[k] = (i0 + k < n) ? (double)w[i0 + k] : -1.0;  // absent
     }
 }
 
-struct ScanOut {
-    double key[VV];    // light: exclusive deficit prefix; heavy: inclusive excess prefix
-    u32 lmask, hmask;  // class bits per item
-    u32 lrank0, hrank0;  // exclusive ranks of this thread's first light/heavy in the tile
-    u32 nl, nh;        // tile counts
-    double totD, totE; // tile totals (upper bounds of all keys)
-};
-
-struct ScanSmem {
-    double wD[NWARP], wE[NWARP];
-    u32 wL[NWARP], wH[NWARP];
-};
-
-// Inclusive warp scan (Kogge-Stone) followed by a running max so the result
-// is non-decreasing whatever the rounding.
+// inclusive Kogge-Stone scan followed by a running max: non-decreasing
 __device__ __forceinline__ double warp_scan_mono(double x, int lane)
 {
 #pragma unroll
@@ -175,82 +170,54 @@ __device__ __forceinline__ double warp_scan_mono(double x, int lane)
     return x;
 }
 
-__device__ __forceinline__ void tile_scan(const double v[VV], double avg, ScanOut &o, ScanSmem &S)
+// Lane-level part of the canonical chunk scan for one class: per-item local
+// prefixes (exclusive for lights, inclusive for heavies), the lane's
+// exclusive base within the chunk and the chunk total.
+template <bool LIGHT>
+__device__ __forceinline__ void lane_class(const double v[VV], double avg, double loc[VV], u32 &mask,
+                                           double &excl, double &total, int lane)
 {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    double ld[VV], le[VV];
-    double sd = 0.0, se = 0.0;
-    u32 lm = 0, hm = 0;
+    double s = 0.0;
+    u32 m = 0;
 #pragma unroll
     for (int k = 0; k < VV; ++k) {
         const bool valid = v[k] >= 0.0;
-        const bool light = valid && v[k] <= avg;
-        const bool heavy = valid && v[k] > avg;
-        ld[k] = sd;                    // exclusive
-        if (light) sd = sd + (avg - v[k]);
-        if (heavy) se = se + (v[k] - avg);
-        le[k] = se;                    // inclusive
-        lm |= (u32)light << k;
-        hm |= (u32)heavy << k;
+        const bool in = LIGHT ? (valid && v[k] <= avg) : (valid && v[k] > avg);
+        if (LIGHT) loc[k] = s;
+        if (in) s = s + (LIGHT ? (avg - v[k]) : (v[k] - avg));
+        if (!LIGHT) loc[k] = s;
+        m |= (u32)in << k;
     }
-    const u32 nlt = __popc(lm), nht = __popc(hm);
-    // lane level
-    double iD = warp_scan_mono(sd, lane), iE = warp_scan_mono(se, lane);
-    double eD = shfl_up_d(iD, 1), eE = shfl_up_d(iE, 1);
-    if (lane == 0) { eD = 0.0; eE = 0.0; }
-    u32 iL = nlt, iH = nht;
+    double inc = warp_scan_mono(s, lane);
+    excl = shfl_up_d(inc, 1);
+    if (lane == 0) excl = 0.0;
+    total = shfl_idx_d(inc, 31);
+    mask = m;
+}
+
+// Canonical keys of one class given the chunk's [base, bound].
+__device__ __forceinline__ void class_keys(double loc[VV], double excl, double base, double bound,
+                                           int lane)
+{
+    double B = fmin(base + excl, bound);
+    double U = __shfl_down_sync(0xffffffffu, B, 1);
+    if (lane == 31) U = bound;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        u32 a = __shfl_up_sync(0xffffffffu, iL, d), b = __shfl_up_sync(0xffffffffu, iH, d);
-        if (lane >= d) { iL += a; iH += b; }
-    }
-    if (lane == 31) { S.wD[wid] = iD; S.wE[wid] = iE; S.wL[wid] = iL; S.wH[wid] = iH; }
-    __syncthreads();
-    // warp level (every warp recomputes the 8-entry scan: no second barrier)
-    double bD = 0.0, bE = 0.0, nD = 0.0, nE = 0.0;
-    u32 bL = 0, bH = 0, tL = 0, tH = 0;
-    {
-        double xD = lane < NWARP ? S.wD[lane] : 0.0, xE = lane < NWARP ? S.wE[lane] : 0.0;
-        double sD = warp_scan_mono(xD, lane), sE = warp_scan_mono(xE, lane);
-        // tile totals: the last warp-inclusive value
-        o.totD = shfl_idx_d(sD, NWARP - 1);
-        o.totE = shfl_idx_d(sE, NWARP - 1);
-        bD = wid ? shfl_idx_d(sD, wid - 1) : 0.0;
-        bE = wid ? shfl_idx_d(sE, wid - 1) : 0.0;
-        nD = shfl_idx_d(sD, wid);  // upper bound for this warp's keys
-        nE = shfl_idx_d(sE, wid);
-        u32 xL = lane < NWARP ? S.wL[lane] : 0, xH = lane < NWARP ? S.wH[lane] : 0;
-#pragma unroll
-        for (int d = 1; d < NWARP; d <<= 1) {
-            u32 a = __shfl_up_sync(0xffffffffu, xL, d), b = __shfl_up_sync(0xffffffffu, xH, d);
-            if (lane >= d) { xL += a; xH += b; }
-        }
-        tL = __shfl_sync(0xffffffffu, xL, NWARP - 1);
-        tH = __shfl_sync(0xffffffffu, xH, NWARP - 1);
-        bL = wid ? __shfl_sync(0xffffffffu, xL, wid - 1) : 0;
-        bH = wid ? __shfl_sync(0xffffffffu, xH, wid - 1) : 0;
-    }
-    // lane bases, clamped into the warp's range; next lane's base = upper bound
-    double BD = fmin(bD + eD, nD), BE = fmin(bE + eE, nE);
-    double UD = __shfl_down_sync(0xffffffffu, BD, 1), UE = __shfl_down_sync(0xffffffffu, BE, 1);
-    if (lane == 31) { UD = nD; UE = nE; }
-#pragma unroll
-    for (int k = 0; k < VV; ++k) {
-        if ((lm >> k) & 1) o.key[k] = fmin(BD + ld[k], UD);
-        else if ((hm >> k) & 1) o.key[k] = fmin(BE + le[k], UE);
-        else o.key[k] = 0.0;
-    }
-    o.lmask = lm;
-    o.hmask = hm;
-    o.lrank0 = bL + iL - nlt;
-    o.hrank0 = bH + iH - nht;
-    o.nl = tL;
-    o.nh = tH;
-    __syncthreads();  // S reusable
+    for (int k = 0; k < VV; ++k) loc[k] = fmin(B + loc[k], U);
+}
+
+// offset of the first set item in the chunk (lane-major), NOFH if none
+__device__ __forceinline__ unsigned char first_item(u32 mask, int lane)
+{
+    unsigned b = __ballot_sync(0xffffffffu, mask != 0);
+    if (!b) return NOFH;
+    int fl = __ffs(b) - 1;
+    u32 fm = __shfl_sync(0xffffffffu, mask, fl);
+    return (unsigned char)(fl * VV + __ffs(fm) - 1);
 }
 
 // ---------------------------------------------------------------------------
-// 1. scan + decoupled look-back
+// 1. scan + super-tile decoupled look-back
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ dd shfl_xor_dd(dd x, int m)
 {
@@ -261,61 +228,125 @@ template <typename T>
 __global__ void __launch_bounds__(TB) k_build_scan(const T *__restrict__ w, u64 n, double avg,
                                                    BuildWs W)
 {
-    __shared__ ScanSmem S;
-    __shared__ unsigned int s_tile;
-    __shared__ unsigned long long s_firstH;
-    __shared__ dd s_exD, s_exH;
-    __shared__ u64 s_exK;
-    if (threadIdx.x == 0) {
-        s_tile = atomicAdd(W.counter, 1u);
-        s_firstH = NONE64;
-    }
+    __shared__ double s_cD[NW], s_cE[NW];
+    __shared__ u32 s_cL[NW];
+    __shared__ unsigned char s_fh[NW];
+    __shared__ double s_tD[SUPER], s_tE[SUPER];
+    __shared__ u32 s_tL[SUPER];
+    __shared__ u64 s_fH[SUPER];
+    __shared__ unsigned int s_st;
+    __shared__ dd s_exD, s_exH, s_agD, s_agH;
+    __shared__ u64 s_exK, s_agK;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_st = atomicAdd(W.counter, 1u);
     __syncthreads();
-    const u64 t = s_tile;
-    const u64 base = t * TILE;
-    double v[VV];
-    load_items(w, n, base, v);
-    ScanOut o;
-    tile_scan(v, avg, o, S);
-    if (o.hmask) {
-        u64 fi = base + (u64)threadIdx.x * VV + (__ffs(o.hmask) - 1);
-        atomicMin(&s_firstH, (unsigned long long)fi);
-    }
-    // publish the aggregate
-    if (threadIdx.x == 0) {
-        W.agg_d[t] = o.totD;
-        W.agg_e[t] = o.totE;
-        W.agg_n[t] = o.nl;
-        __threadfence();
-        st_release_u32(&W.status[t], t == 0 ? 2u : 1u);
-        if (t == 0) {  // tile 0 is its own inclusive prefix
-            W.inc_D[0] = dd_make(o.totD);
-            W.inc_H[0] = dd_make(o.totE);
-            W.inc_k[0] = o.nl;
-            __threadfence();
-            st_release_u32(&W.status[0], 2u);
+    const u64 st = s_st;
+    const u64 t0 = st * SUPER;
+    const u64 tn = (t0 + SUPER <= W.nt) ? SUPER : W.nt - t0;
+
+    double vnext[VV];
+    load8(w, n, t0 * TILE + (u64)threadIdx.x * VV, vnext);
+    for (u64 j = 0; j < tn; ++j) {
+        const u64 t = t0 + j;
+        double v[VV];
+#pragma unroll
+        for (int k = 0; k < VV; ++k) v[k] = vnext[k];
+        if (j + 1 < tn) load8(w, n, (t + 1) * TILE + (u64)threadIdx.x * VV, vnext);
+        double loc[VV], ex, totD, totE;
+        u32 lm, hm;
+        lane_class<true>(v, avg, loc, lm, ex, totD, lane);
+        lane_class<false>(v, avg, loc, hm, ex, totE, lane);
+        u32 nl = __popc(lm);
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) nl += __shfl_xor_sync(0xffffffffu, nl, d);
+        const unsigned char fh = first_item(hm, lane);
+        if (lane == 0) {
+            s_cD[wid] = totD;
+            s_cE[wid] = totE;
+            s_cL[wid] = nl;
+            s_fh[wid] = fh;
         }
+        __syncthreads();
+        if (wid == 0) {
+            // monotone scan of the chunk totals -> chunk bounds
+            double x = lane < NW ? s_cD[lane] : 0.0, y = lane < NW ? s_cE[lane] : 0.0;
+#pragma unroll
+            for (int d = 1; d < NW; d <<= 1) {
+                double a = shfl_up_d(x, d), b = shfl_up_d(y, d);
+                if (lane >= d) { x = x + a; y = y + b; }
+            }
+#pragma unroll
+            for (int d = 1; d < NW; d <<= 1) {
+                double a = shfl_up_d(x, d), b = shfl_up_d(y, d);
+                if (lane >= d) { x = fmax(x, a); y = fmax(y, b); }
+            }
+            const unsigned char f = lane < NW ? s_fh[lane] : NOFH;
+            if (lane < NW) {
+                W.mD[t * NW + lane] = x;
+                W.mE[t * NW + lane] = y;
+                W.mfh[t * NW + lane] = f;
+            }
+            u32 cl = lane < NW ? s_cL[lane] : 0;
+#pragma unroll
+            for (int d = 16; d >= 1; d >>= 1) cl += __shfl_xor_sync(0xffffffffu, cl, d);
+            unsigned fhm = __ballot_sync(0xffffffffu, lane < NW && f != NOFH);
+            const int c = fhm ? __ffs(fhm) - 1 : 0;
+            const unsigned char fc = (unsigned char)__shfl_sync(0xffffffffu, (int)f, c);
+            if (lane == NW - 1) {
+                s_tD[j] = x;
+                s_tE[j] = y;
+            }
+            if (lane == 0) {
+                s_tL[j] = cl;
+                s_fH[j] = fhm ? t * TILE + (u64)c * CH + fc : NONE64;
+            }
+        }
+        __syncthreads();
     }
-    // warp 0 looks back
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
+    // super-tile aggregate: exact double-double sum of the tile totals
+    if (threadIdx.x == 0) {
         dd aD = dd_make(0.0), aH = dd_make(0.0);
         u64 aK = 0;
-        i64 pred = (i64)t - 1;
+        for (u64 j = 0; j < tn; ++j) {
+            aD = dd_add_d(aD, s_tD[j]);
+            aH = dd_add_d(aH, s_tE[j]);
+            aK += s_tL[j];
+        }
+        s_agD = aD;
+        s_agH = aH;
+        s_agK = aK;
+        if (st == 0) {
+            W.inc_D[0] = aD;
+            W.inc_H[0] = aH;
+            W.inc_k[0] = aK;
+        } else {
+            W.agg_D[st] = aD;
+            W.agg_H[st] = aH;
+            W.agg_k[st] = aK;
+        }
+        __threadfence();
+        st_release_u32(&W.status[st], st == 0 ? 2u : 1u);
+    }
+    __syncthreads();
+    // look-back by warp 0
+    if (threadIdx.x < 32) {
+        dd aD = dd_make(0.0), aH = dd_make(0.0);
+        u64 aK = 0;
+        i64 pred = (i64)st - 1;
         while (pred >= 0) {
-            i64 p = pred - lane;
-            u32 st = 2;
+            const i64 p = pred - lane;
+            u32 s = 2;
             if (p >= 0) {
-                do { st = ld_acquire_u32(&W.status[p]); } while (st == 0);
+                do { s = ld_acquire_u32(&W.status[p]); } while (s == 0);
             }
-            unsigned inc_mask = __ballot_sync(0xffffffffu, p >= 0 && st == 2);
-            int stop = inc_mask ? __ffs(inc_mask) - 1 : 32;  // first lane with an inclusive
+            const unsigned inc_mask = __ballot_sync(0xffffffffu, p >= 0 && s == 2);
+            const int stop = inc_mask ? __ffs(inc_mask) - 1 : 32;
             dd cD = dd_make(0.0), cH = dd_make(0.0);
             u64 cK = 0;
             if (p >= 0 && lane < stop) {
-                cD = dd_make(W.agg_d[p]);
-                cH = dd_make(W.agg_e[p]);
-                cK = W.agg_n[p];
+                cD = W.agg_D[p];
+                cH = W.agg_H[p];
+                cK = W.agg_k[p];
             } else if (p >= 0 && lane == stop) {
                 cD = W.inc_D[p];
                 cH = W.inc_H[p];
@@ -334,12 +365,12 @@ __global__ void __launch_bounds__(TB) k_build_scan(const T *__restrict__ w, u64 
             pred -= 32;
         }
         if (lane == 0) {
-            if (t > 0) {
-                W.inc_D[t] = dd_add_d(aD, o.totD);
-                W.inc_H[t] = dd_add_d(aH, o.totE);
-                W.inc_k[t] = aK + o.nl;
+            if (st > 0) {
+                W.inc_D[st] = dd_add(aD, s_agD);
+                W.inc_H[st] = dd_add(aH, s_agH);
+                W.inc_k[st] = aK + s_agK;
                 __threadfence();
-                st_release_u32(&W.status[t], 2u);
+                st_release_u32(&W.status[st], 2u);
             }
             s_exD = aD;
             s_exH = aH;
@@ -347,15 +378,24 @@ __global__ void __launch_bounds__(TB) k_build_scan(const T *__restrict__ w, u64 
         }
     }
     __syncthreads();
+    // exclusive bases of the super-tile's tiles
     if (threadIdx.x == 0) {
-        W.DLb[t] = s_exD;
-        W.DHb[t] = s_exH;
-        W.kL[t] = s_exK;
-        W.firstH[t] = s_firstH;
-        if (t == W.nt - 1) {
-            W.DLb[W.nt] = dd_add_d(s_exD, o.totD);
-            W.DHb[W.nt] = dd_add_d(s_exH, o.totE);
-            W.kL[W.nt] = s_exK + o.nl;
+        dd D = s_exD, H = s_exH;
+        u64 K = s_exK;
+        for (u64 j = 0; j < tn; ++j) {
+            const u64 t = t0 + j;
+            W.DLb[t] = D;
+            W.DHb[t] = H;
+            W.kL[t] = K;
+            W.firstH[t] = s_fH[j];
+            D = dd_add_d(D, s_tD[j]);
+            H = dd_add_d(H, s_tE[j]);
+            K += s_tL[j];
+        }
+        if (t0 + tn == W.nt) {
+            W.DLb[W.nt] = D;
+            W.DHb[W.nt] = H;
+            W.kL[W.nt] = K;
         }
     }
 }
@@ -368,10 +408,9 @@ __global__ void k_build_coarse(BuildWs W, u64 n)
     const u64 nt = W.nt;
     u64 u = (u64)blockIdx.x * blockDim.x + threadIdx.x;
     if (u > nt) return;
-    // T1[u] = max{t in [0, nt] : DHb[t] <= DLb[u]}
-    {
+    {  // T1[u] = max{t in [0, nt] : DHb[t] <= DLb[u]}
         const dd x = W.DLb[u];
-        u64 lo = 0, hi = nt;  // DHb[0] = 0 <= x always
+        u64 lo = 0, hi = nt;
         while (lo < hi) {
             u64 mid = (lo + hi + 1) >> 1;
             if (dd_le(W.DHb[mid], x)) lo = mid;
@@ -379,13 +418,12 @@ __global__ void k_build_coarse(BuildWs W, u64 n)
         }
         W.T1[u] = (u32)lo;
     }
-    // S1[u] = max{s in [0, nt] : DLb[s] < DHb[u]}, 0 if none
-    {
+    {  // S1[u] = max{s in [0, nt] : DLb[s] < DHb[u]}, 0 if none
         const dd y = W.DHb[u];
-        u64 lo = 0, hi = nt;
         if (!dd_lt(W.DLb[0], y)) {
             W.S1[u] = 0;
         } else {
+            u64 lo = 0, hi = nt;
             while (lo < hi) {
                 u64 mid = (lo + hi + 1) >> 1;
                 if (dd_lt(W.DLb[mid], y)) lo = mid;
@@ -394,9 +432,8 @@ __global__ void k_build_coarse(BuildWs W, u64 n)
             W.S1[u] = (u32)lo;
         }
     }
-    // nextH[u]: first heavy item in tiles > u
-    if (u < nt) {
-        auto jH = [&](u64 t) -> u64 {  // heavies before tile t
+    if (u < nt) {  // nextH[u]: first heavy item in tiles > u
+        auto jH = [&](u64 t) -> u64 {
             u64 items = t * TILE < n ? t * TILE : n;
             return items - W.kL[t];
         };
@@ -404,7 +441,7 @@ __global__ void k_build_coarse(BuildWs W, u64 n)
         if (jH(nt) <= after) {
             W.nextH[u] = NONE64;
         } else {
-            u64 lo = u + 1, hi = nt - 1;  // smallest t with jH(t+1) > after
+            u64 lo = u + 1, hi = nt - 1;
             while (lo < hi) {
                 u64 mid = (lo + hi) >> 1;
                 if (jH(mid + 1) > after) hi = mid;
@@ -416,256 +453,258 @@ __global__ void k_build_coarse(BuildWs W, u64 n)
 }
 
 // ---------------------------------------------------------------------------
-// 3. tile-owner pack
+// 3. warp-per-chunk pack
 // ---------------------------------------------------------------------------
-template <typename T> struct PackSmem {
-    double ownLk[TILE];
-    double ownHk[TILE];
-    double fk[TILE];
-    u32 fidx[TILE];
-    unsigned short ownLp[TILE];
-    unsigned short ownHp[TILE];
-    typename RowOf<T>::type rows[TILE];
-    ScanSmem S;
-    u32 nLo, nHo, nF;
-    u32 r_next;
-    u64 tile_sel;
+template <typename T> struct WarpSmem {
+    double K[CH];   // own keys: lights [0, nL), heavies [nL, nL + nH)
+    double F[CH];   // keys of one class of one foreign chunk
+    typename RowOf<T>::type R[CH];
+    unsigned char P[CH];
+    unsigned char FP[CH];
 };
 
-// compact one class of tile t into (fk, fidx); lights if want_light
-template <typename T>
-__device__ void load_foreign(const T *__restrict__ w, u64 n, double avg, u64 t, bool want_light,
-                             PackSmem<T> &P)
+// d + x as a normalised double-double (exact for the key ranges in play)
+__device__ __forceinline__ dd add_dd_d(dd d, double x)
 {
-    double v[VV];
-    load_items(w, n, t * TILE, v);
-    ScanOut o;
-    tile_scan(v, avg, o, P.S);
-    u32 m = want_light ? o.lmask : o.hmask;
-    u32 r = want_light ? o.lrank0 : o.hrank0;
-#pragma unroll
-    for (int k = 0; k < VV; ++k) {
-        if ((m >> k) & 1) {
-            P.fk[r] = o.key[k];
-            P.fidx[r] = (u32)(threadIdx.x * VV + k);
-            ++r;
-        }
+    double s, e;
+    two_sum(d.hi, x, s, e);
+    e += d.lo;
+    double h, l;
+    fast_two_sum(s, e, h, l);
+    return dd_make(h, l);
+}
+// f <= X and f < X for normalised X
+__device__ __forceinline__ bool le_d_dd(double f, dd X) { return f < X.hi || (f == X.hi && X.lo >= 0.0); }
+__device__ __forceinline__ bool lt_d_dd(double f, dd X) { return f < X.hi || (f == X.hi && X.lo > 0.0); }
+
+// first heavy item (0-based) after chunk c of tile t, NONE64 if none;
+// fh_lane = mfh[t*8 + lane] on lanes < 8
+__device__ __forceinline__ u64 next_heavy_after(const BuildWs &W, u64 t, int c,
+                                                unsigned char fh_lane, int lane)
+{
+    unsigned m = __ballot_sync(0xffffffffu, lane < NW && lane > c && fh_lane != NOFH);
+    if (m) {
+        int cc = __ffs(m) - 1;
+        unsigned char f = (unsigned char)__shfl_sync(0xffffffffu, (int)fh_lane, cc);
+        return t * TILE + (u64)cc * CH + f;
     }
-    if (threadIdx.x == 0) P.nF = want_light ? o.nl : o.nh;
-    __syncthreads();
+    return W.nextH[t];
+}
+
+// compact one class of foreign chunk (tile t, chunk c) into S.F / S.FP
+template <typename T, bool LIGHT>
+__device__ __forceinline__ u32 foreign_chunk(const T *__restrict__ w, u64 n, double avg, u64 fb,
+                                             double base, double bound, WarpSmem<T> &S, int lane)
+{
+    double fv[VV], fk[VV], fex, ftot;
+    u32 fm;
+    load8(w, n, fb + (u64)lane * VV, fv);
+    lane_class<LIGHT>(fv, avg, fk, fm, fex, ftot, lane);
+    class_keys(fk, fex, base, bound, lane);
+    const u32 fc = __popc(fm);
+    u32 fi = fc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        u32 a = __shfl_up_sync(0xffffffffu, fi, d);
+        if (lane >= d) fi += a;
+    }
+    const u32 nF = __shfl_sync(0xffffffffu, fi, 31);
+    __syncwarp();
+    u32 rr = fi - fc;
+#pragma unroll
+    for (int k = 0; k < VV; ++k)
+        if ((fm >> k) & 1) {
+            S.F[rr] = fk[k];
+            if (!LIGHT) S.FP[rr] = (unsigned char)(lane * VV + k);
+            ++rr;
+        }
+    __syncwarp();
+    return nF;
 }
 
 template <typename T>
-__global__ void __launch_bounds__(TB) k_build_pack(const T *__restrict__ w, u64 n, double avg,
-                                                   BuildWs W,
-                                                   typename RowOf<T>::type *__restrict__ rows_out)
+__global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u64 n, double avg,
+                                                      BuildWs W,
+                                                      typename RowOf<T>::type *__restrict__ rows_out)
 {
-    extern __shared__ __align__(16) unsigned char pack_smem[];
-    PackSmem<T> &P = *reinterpret_cast<PackSmem<T> *>(pack_smem);
     typedef typename RowOf<T>::type RowT;
     typedef decltype(RowT::alias) AliasT;
-    const u64 u = blockIdx.x;
+    extern __shared__ __align__(16) unsigned char pack_smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    WarpSmem<T> &S = reinterpret_cast<WarpSmem<T> *>(pack_smem)[wid];
     const u64 nt = W.nt;
-    const u64 base = u * TILE;
-    const u32 items = (u32)((n - base) < (u64)TILE ? (n - base) : (u64)TILE);
+    const u64 u = blockIdx.x;
+    const u64 cbase = u * TILE + (u64)wid * CH;  // first item of this chunk
+    if (cbase >= n) return;
 
-    // --- own tile: keys, compaction, light thresholds, heavy aliases
+    // ---- own chunk: canonical keys of both classes
     double v[VV];
-    load_items(w, n, base, v);
-    ScanOut o;
-    tile_scan(v, avg, o, P.S);
+    load8(w, n, cbase + (u64)lane * VV, v);
+    const double bD0 = wid ? W.mD[u * NW + wid - 1] : 0.0, bD1 = W.mD[u * NW + wid];
+    const double bE0 = wid ? W.mE[u * NW + wid - 1] : 0.0, bE1 = W.mE[u * NW + wid];
+    const unsigned char fh_own = lane < NW ? W.mfh[u * NW + lane] : NOFH;
+    const dd DLu = W.DLb[u], DHu = W.DHb[u];
+    u32 lm, hm, nL, nH;
     {
-        u32 rl = o.lrank0, rh = o.hrank0;
+        double kD[VV], kE[VV], exD, exE, tD, tE;
+        lane_class<true>(v, avg, kD, lm, exD, tD, lane);
+        lane_class<false>(v, avg, kE, hm, exE, tE, lane);
+        class_keys(kD, exD, bD0, bD1, lane);
+        class_keys(kE, exE, bE0, bE1, lane);
+        const u32 cl = __popc(lm), chh = __popc(hm);
+        u32 il = cl, ih = chh;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            u32 a = __shfl_up_sync(0xffffffffu, il, d), b = __shfl_up_sync(0xffffffffu, ih, d);
+            if (lane >= d) { il += a; ih += b; }
+        }
+        nL = __shfl_sync(0xffffffffu, il, 31);
+        nH = __shfl_sync(0xffffffffu, ih, 31);
+        u32 rl = il - cl, rh = nL + ih - chh;
 #pragma unroll
         for (int k = 0; k < VV; ++k) {
-            const u32 pos = threadIdx.x * VV + k;
-            if ((o.lmask >> k) & 1) {
-                P.ownLk[rl] = o.key[k];
-                P.ownLp[rl] = (unsigned short)pos;
-                P.rows[pos].tw = (T)v[k];
+            const u32 pos = lane * VV + k;
+            if ((lm >> k) & 1) {
+                S.K[rl] = kD[k];
+                S.P[rl] = (unsigned char)pos;
+                S.R[pos].tw = (decltype(RowT::tw))v[k];
                 ++rl;
-            } else if ((o.hmask >> k) & 1) {
-                P.ownHk[rh] = o.key[k];
-                P.ownHp[rh] = (unsigned short)pos;
+            } else if ((hm >> k) & 1) {
+                S.K[rh] = kE[k];
+                S.P[rh] = (unsigned char)pos;
                 ++rh;
             }
         }
-        if (threadIdx.x == 0) {
-            P.nLo = o.nl;
-            P.nHo = o.nh;
-        }
     }
-    __syncthreads();
-    const u32 nLo = P.nLo, nHo = P.nHo;
-    const dd DLu = W.DLb[u], DHu = W.DHb[u];
-    // heavy aliases: next heavy in the tile, or the first heavy after it
+    __syncwarp();
+    // heavy aliases: next heavy in the chunk, else after the chunk
     {
-        const u64 nxt = W.nextH[u];
-        for (u32 r = threadIdx.x; r < nHo; r += TB) {
-            const u32 pos = P.ownHp[r];
+        const u64 after = next_heavy_after(W, u, wid, fh_own, lane);
+        for (u32 r = lane; r < nH; r += 32) {
+            const u32 pos = S.P[nL + r];
             u64 a;
-            if (r + 1 < nHo) a = base + P.ownHp[r + 1] + 1;
-            else a = (nxt == NONE64) ? base + pos + 1 : nxt + 1;
-            P.rows[pos].alias = (AliasT)a;
+            if (r + 1 < nH) a = cbase + S.P[nL + r + 1] + 1;
+            else a = (after == NONE64) ? cbase + pos + 1 : after + 1;
+            S.R[pos].alias = (AliasT)a;
         }
     }
 
-    // --- lights: alias = first heavy with key > light key
-    {
-        u64 cur = W.T1[u];  // DHb[cur] <= DLu <= every own light key
+    // ---- lights: alias = first heavy (in key order) with key > light key
+    if (nL) {
         u32 r0 = 0;
-        while (r0 < nLo) {
-            // t = max{t >= cur : DHb[t] <= DLu + lk[r0]}  (gallop, then bisect)
-            if (threadIdx.x == 0) {
-                const dd x = dd_make(P.ownLk[r0]);
-                u64 lo = cur, step = 1;
-                while (lo + step <= nt && dd_le(dd_sub(W.DHb[lo + step], DLu), x)) {
-                    lo += step;
-                    step <<= 1;
-                }
-                u64 hi = lo + step - 1 < nt ? lo + step - 1 : nt;
-                while (lo < hi) {
-                    u64 mid = (lo + hi + 1) >> 1;
-                    if (dd_le(dd_sub(W.DHb[mid], DLu), x)) lo = mid;
-                    else hi = mid - 1;
-                }
-                P.tile_sel = lo;
-            }
-            __syncthreads();
-            const u64 t = P.tile_sel;
+        const u64 tA = W.T1[u], tB = W.T1[u + 1];
+        for (u64 t = tA; t <= tB && r0 < nL; ++t) {
             if (t >= nt) {
-                // no heavy key above: the remaining lights keep their own rows
-                for (u32 r = r0 + threadIdx.x; r < nLo; r += TB) {
-                    const u32 pos = P.ownLp[r];
-                    P.rows[pos].alias = (AliasT)(base + pos + 1);
+                for (u32 r = r0 + lane; r < nL; r += 32) {
+                    const u32 pos = S.P[r];
+                    S.R[pos].alias = (AliasT)(cbase + pos + 1);
                 }
-                __syncthreads();
+                r0 = nL;
                 break;
             }
-            const double *hk;
-            const u32 *hpos = nullptr;
-            u32 nF;
-            const u64 tbase = t * TILE;
-            if (t == u) {
-                hk = P.ownHk;
-                nF = nHo;
-            } else {
-                load_foreign(w, n, avg, t, false, P);
-                hk = P.fk;
-                nF = P.nF;
-                hpos = P.fidx;
-            }
-            const u64 after_t = W.nextH[t];
-            const dd lim = dd_sub(W.DHb[t + 1], DLu);  // resolved here: lk < lim
-            const dd Dlt = dd_sub(DLu, W.DHb[t]);      // heavy m <= light  <=>  hk - lk <= Dlt
-            if (threadIdx.x == 0) {
-                u32 lo = r0 + 1, hi = nLo;  // r0 itself is resolved here
+            const dd Dl = dd_sub(DLu, W.DHb[t]);  // heavy (rel t) <= light (rel u): hk <= lk + Dl
+            const double mE_l = lane < NW ? W.mE[t * NW + lane] : 0.0;
+            const unsigned char fh_l = lane < NW ? W.mfh[t * NW + lane] : NOFH;
+            for (int c = 0; c < NW && r0 < nL; ++c) {
+                const double bnd = __shfl_sync(0xffffffffu, mE_l, c);
+                // lights resolved by chunk c: lk + Dl < bnd
+                u32 lo = r0, hi = nL;
                 while (lo < hi) {
                     u32 mid = (lo + hi) >> 1;
-                    if (dd_lt(dd_make(P.ownLk[mid]), lim)) lo = mid + 1;
+                    if (!le_d_dd(bnd, add_dd_d(Dl, S.K[mid]))) lo = mid + 1;
                     else hi = mid;
                 }
-                P.r_next = lo;
-            }
-            __syncthreads();
-            const u32 r1 = P.r_next;
-            for (u32 r = r0 + threadIdx.x; r < r1; r += TB) {
-                const double lk = P.ownLk[r];
-                u32 lo = 0, hi = nF;  // first heavy m with key > light key
-                while (lo < hi) {
-                    u32 mid = (lo + hi) >> 1;
-                    if (diff_le(hk[mid], lk, Dlt)) lo = mid + 1;
-                    else hi = mid;
+                const u32 r1 = lo;
+                if (r1 == r0) continue;
+                const u64 fb = t * TILE + (u64)c * CH;
+                const double b0 = c ? __shfl_sync(0xffffffffu, mE_l, c - 1) : 0.0;
+                const u32 nF = foreign_chunk<T, false>(w, n, avg, fb, b0, bnd, S, lane);
+                const u64 after = next_heavy_after(W, t, c, fh_l, lane);
+                for (u32 r = r0 + lane; r < r1; r += 32) {
+                    const dd X = add_dd_d(Dl, S.K[r]);
+                    u32 a = 0, b = nF;  // first m with F[m] > X
+                    while (a < b) {
+                        u32 mid = (a + b) >> 1;
+                        if (le_d_dd(S.F[mid], X)) a = mid + 1;
+                        else b = mid;
+                    }
+                    const u32 pos = S.P[r];
+                    u64 al;
+                    if (a < nF) al = fb + S.FP[a] + 1;
+                    else al = (after == NONE64) ? cbase + pos + 1 : after + 1;
+                    S.R[pos].alias = (AliasT)al;
                 }
-                const u32 pos = P.ownLp[r];
-                u64 a;
-                if (lo < nF) a = tbase + (hpos ? hpos[lo] : P.ownHp[lo]) + 1;
-                else a = (after_t == NONE64) ? base + pos + 1 : after_t + 1;
-                P.rows[pos].alias = (AliasT)a;
+                __syncwarp();
+                r0 = r1;
             }
-            __syncthreads();
-            r0 = r1;
-            cur = t + 1;
+        }
+        // defensive: lights left over (inconsistent bounds) keep their own row
+        for (u32 r = r0 + lane; r < nL; r += 32) {
+            const u32 pos = S.P[r];
+            S.R[pos].alias = (AliasT)(cbase + pos + 1);
         }
     }
 
-    // --- heavies: tw = key - DL(first light with key >= heavy key) + avg
-    {
-        u64 cur = W.S1[u];  // DLb[cur] < every own heavy key (or cur = 0)
+    // ---- heavies: tw = key - DL(first light with key >= heavy key) + avg
+    if (nH) {
         u32 r0 = 0;
-        while (r0 < nHo) {
-            // s = max{s >= cur : DLb[s] < DHu + hk[r0]}
-            if (threadIdx.x == 0) {
-                const dd y = dd_make(P.ownHk[r0]);
-                u64 lo = cur, step = 1;
-                while (lo + step <= nt && dd_lt(dd_sub(W.DLb[lo + step], DHu), y)) {
-                    lo += step;
-                    step <<= 1;
-                }
-                u64 hi = lo + step - 1 < nt ? lo + step - 1 : nt;
-                while (lo < hi) {
-                    u64 mid = (lo + hi + 1) >> 1;
-                    if (dd_lt(dd_sub(W.DLb[mid], DHu), y)) lo = mid;
-                    else hi = mid - 1;
-                }
-                P.tile_sel = lo;
-            }
-            __syncthreads();
-            const u64 s = P.tile_sel;
-            if (s >= nt) {
-                // no light key >= heavy key: DL = total deficit
-                const dd A = dd_sub(DHu, W.DLb[nt]);
-                for (u32 r = r0 + threadIdx.x; r < nHo; r += TB) {
-                    dd tw = dd_add_d(dd_add_d(A, P.ownHk[r]), avg);
-                    P.rows[P.ownHp[r]].tw = tw_store<T>(tw.hi + tw.lo, avg);
-                }
-                __syncthreads();
-                break;
-            }
-            const double *lk;
-            u32 nF;
-            if (s == u) {
-                lk = P.ownLk;
-                nF = nLo;
-            } else {
-                load_foreign(w, n, avg, s, true, P);
-                lk = P.fk;
-                nF = P.nF;
-            }
-            const dd lim = dd_sub(W.DLb[s + 1], DHu);  // resolved here: hk <= lim
-            const dd Dhs = dd_sub(DHu, W.DLb[s]);      // light m < heavy  <=>  lk - hk < Dhs
-            const dd Aend = dd_sub(DHu, W.DLb[s + 1]);
-            if (threadIdx.x == 0) {
-                u32 lo = r0 + 1, hi = nHo;
+        const u64 sA = W.S1[u], sB = W.S1[u + 1];
+        const double *HK = S.K + nL;
+        const unsigned char *HP = S.P + nL;
+        for (u64 s = sA; s <= sB && r0 < nH; ++s) {
+            if (s >= nt) break;
+            const dd Dh = dd_sub(DHu, W.DLb[s]);  // light (rel s) < heavy (rel u): lk < hk + Dh
+            const double mD_l = lane < NW ? W.mD[s * NW + lane] : 0.0;
+            for (int c = 0; c < NW && r0 < nH; ++c) {
+                const double bnd = __shfl_sync(0xffffffffu, mD_l, c);
+                // heavies resolved by chunk c: hk + Dh <= bnd
+                u32 lo = r0, hi = nH;
                 while (lo < hi) {
                     u32 mid = (lo + hi) >> 1;
-                    if (dd_le(dd_make(P.ownHk[mid]), lim)) lo = mid + 1;
+                    if (!lt_d_dd(bnd, add_dd_d(Dh, HK[mid]))) lo = mid + 1;
                     else hi = mid;
                 }
-                P.r_next = lo;
-            }
-            __syncthreads();
-            const u32 r1 = P.r_next;
-            for (u32 r = r0 + threadIdx.x; r < r1; r += TB) {
-                const double hk = P.ownHk[r];
-                u32 lo = 0, hi = nF;  // first light m with key >= heavy key
-                while (lo < hi) {
-                    u32 mid = (lo + hi) >> 1;
-                    if (dd_lt(two_diff_dd(lk[mid], hk), Dhs)) lo = mid + 1;
-                    else hi = mid;
+                const u32 r1 = lo;
+                if (r1 == r0) continue;
+                const u64 fb = s * TILE + (u64)c * CH;
+                const double b0 = c ? __shfl_sync(0xffffffffu, mD_l, c - 1) : 0.0;
+                const u32 nF = foreign_chunk<T, true>(w, n, avg, fb, b0, bnd, S, lane);
+                for (u32 r = r0 + lane; r < r1; r += 32) {
+                    const dd Y = add_dd_d(Dh, HK[r]);
+                    u32 a = 0, b = nF;  // first m with F[m] >= Y
+                    while (a < b) {
+                        u32 mid = (a + b) >> 1;
+                        if (lt_d_dd(S.F[mid], Y)) a = mid + 1;
+                        else b = mid;
+                    }
+                    const double DL = a < nF ? S.F[a] : bnd;  // rel s
+                    // tw = (DHu + hk) - (DLb[s] + DL) + avg = Y - DL + avg
+                    const dd tw = dd_add_d(add_dd_d(Y, -DL), avg);
+                    S.R[HP[r]].tw = tw_store<T>(tw.hi + tw.lo, avg);
                 }
-                dd tw = (lo < nF) ? dd_add(Dhs, two_diff_dd(hk, lk[lo])) : dd_add_d(Aend, hk);
-                tw = dd_add_d(tw, avg);
-                P.rows[P.ownHp[r]].tw = tw_store<T>(tw.hi + tw.lo, avg);
+                __syncwarp();
+                r0 = r1;
             }
-            __syncthreads();
-            r0 = r1;
-            cur = s + 1;
+        }
+        // heavies above every light key: DL = the total deficit
+        const dd A = dd_sub(DHu, W.DLb[nt]);
+        for (u32 r = r0 + lane; r < nH; r += 32) {
+            const dd tw = dd_add_d(add_dd_d(A, HK[r]), avg);
+            S.R[HP[r]].tw = tw_store<T>(tw.hi + tw.lo, avg);
         }
     }
-    __syncthreads();
-    RowT *dst = rows_out + base;
-    for (u32 i = threadIdx.x; i < items; i += TB) dst[i] = P.rows[i];
+    __syncwarp();
+    // ---- store the chunk's rows (each lane its 8 consecutive rows)
+    const u64 i0 = cbase + (u64)lane * VV;
+    if (i0 + VV <= n) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(&S.R[lane * VV]);
+        uint4 *dst = reinterpret_cast<uint4 *>(rows_out + i0);
+#pragma unroll
+        for (int q = 0; q < (int)(VV * sizeof(RowT) / 16); ++q) dst[q] = src[q];
+    } else {
+        for (int k = 0; k < VV; ++k)
+            if (i0 + k < n) rows_out[i0 + k] = S.R[lane * VV + k];
+    }
 }
 
 template <typename T>
@@ -675,16 +714,15 @@ int run_build(const void *wv, u64 n, double total, void *rows, void *ws, cudaStr
     BuildWs W = carve(ws, n);
     const double avg = total / (double)n;
     AK_CUDA_TRY(cudaMemsetAsync(W.counter, 0, 256, st));
-    AK_CUDA_TRY(cudaMemsetAsync(W.status, 0, W.nt * 4, st));
-    k_build_scan<T><<<(unsigned)W.nt, TB, 0, st>>>(w, n, avg, W);
+    AK_CUDA_TRY(cudaMemsetAsync(W.status, 0, W.nst * 4, st));
+    k_build_scan<T><<<(unsigned)W.nst, TB, 0, st>>>(w, n, avg, W);
     AK_LAUNCH_CHECK("k_build_scan");
     k_build_coarse<<<(unsigned)((W.nt + 1 + 255) / 256), 256, 0, st>>>(W, n);
     AK_LAUNCH_CHECK("k_build_coarse");
-    size_t smem = sizeof(PackSmem<T>);
+    const size_t smem = sizeof(WarpSmem<T>) * NW;
     AK_CUDA_TRY(cudaFuncSetAttribute(k_build_pack<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-    k_build_pack<T><<<(unsigned)W.nt, TB, smem, st>>>(w, n, avg, W,
-                                                      (typename RowOf<T>::type *)rows);
+    k_build_pack<T><<<(unsigned)W.nt, TB, smem, st>>>(w, n, avg, W, (typename RowOf<T>::type *)rows);
     AK_LAUNCH_CHECK("k_build_pack");
     return AK_OK;
 }
@@ -704,7 +742,7 @@ int ak_build_psa(const void *w, int dtype, uint64_t n, double total, void *rows,
 {
     if (n == 0) return AK_ERR_EMPTY_INPUT;
     if (ws_bytes < ws_bytes_for(n)) return AK_ERR_WORKSPACE;
-    if (((uintptr_t)w & 15) != 0) return AK_ERR_VALUE;
+    if (((uintptr_t)w & 15) != 0 || ((uintptr_t)rows & 15) != 0) return AK_ERR_VALUE;
     cudaStream_t st = ak_stream(stream);
     if (dtype == AK_F32) {
         if (n >= 0xFFFFFFFFull) return AK_ERR_VALUE;  // u32 aliases

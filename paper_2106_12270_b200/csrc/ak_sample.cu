@@ -149,6 +149,82 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, u32 bytes, 
         : "memory");
 }
 
+// Philox2x64-10 with a precomputed key schedule (the per-round keys depend
+// on the seed only, so they are hoisted out of the draw loop).
+struct KeySched64 {
+    u64 k[10];
+};
+__device__ __forceinline__ KeySched64 sched64(u64 key)
+{
+    KeySched64 s;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) s.k[r] = key + (u64)r * AK_PHILOX_WEYL;
+    return s;
+}
+__device__ __forceinline__ u64 philox64_sched(u64 x0, u64 x1, const KeySched64 &s)
+{
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        u64 hi = __umul64hi(x0, AK_PHILOX_MULT);
+        u64 lo = x0 * AK_PHILOX_MULT;
+        x0 = hi ^ s.k[r] ^ x1;
+        x1 = lo;
+    }
+    return x0;
+}
+struct KeySched32 {
+    uint2 k[10];
+};
+__device__ __forceinline__ KeySched32 sched32(u64 seed)
+{
+    KeySched32 s;
+    uint2 k = make_uint2((u32)seed, (u32)(seed >> 32));
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        s.k[r] = k;
+        k.x += AK_PH4_W0;
+        k.y += AK_PH4_W1;
+    }
+    return s;
+}
+__device__ __forceinline__ void philox32_sched(u64 call, u64 strm, const KeySched32 &s, u64 &a, u64 &b)
+{
+    uint4 c = make_uint4((u32)call, (u32)(call >> 32), (u32)strm, (u32)(strm >> 32));
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        u32 hi0 = __umulhi(AK_PH4_M0, c.x), lo0 = AK_PH4_M0 * c.x;
+        u32 hi1 = __umulhi(AK_PH4_M1, c.z), lo1 = AK_PH4_M1 * c.z;
+        c = make_uint4(hi1 ^ c.y ^ s.k[r].x, lo1, hi0 ^ c.w ^ s.k[r].y, lo0);
+    }
+    a = ((u64)c.y << 32) | c.x;
+    b = ((u64)c.w << 32) | c.z;
+}
+
+// The bucket rule from a raw 64-bit word.  For a power-of-two span 2^b the
+// reference's f64 steps x = u*span, k = trunc(x), x - k (span >= 2) are exact bit
+// manipulations: k = word >> (64-b), x - k = low 53-b bits of (word >> 11)
+// scaled by 2^(b-53) (built as 1.f - 1.0, exact) — bit-identical results
+// with four fewer double operations.  Other spans use the f64 rule.
+template <typename RowT>
+__device__ __forceinline__ i64 rule_word(const RowT *tab, u64 word, i64 span, int b, bool pow2,
+                                         i64 lo, double avg)
+{
+    i64 k;
+    double frac;
+    if (pow2) {
+        k = (i64)(word >> (64 - b));
+        const u64 f = (word >> 11) & ((1ull << (53 - b)) - 1);  // 53-b fraction bits
+        frac = __longlong_as_double((long long)(0x3FF0000000000000ull | (f << (b - 1)))) - 1.0;
+    } else {
+        const double x = ak_u53(word) * (double)span;
+        k = (i64)x;
+        if (k >= span) k = span - 1;
+        frac = x - (double)k;
+    }
+    const RowT r = tab[k];
+    return (frac * avg < (double)r.tw) ? (lo + k + 1) : (i64)r.alias;
+}
+
 // One CTA per section (grid-strided over [first, first+count)); the rows of
 // the section are copied into shared memory once, then every draw of the
 // section reads its row from there.  STAGE=false reads rows from global
@@ -168,6 +244,8 @@ __global__ void __launch_bounds__(1024) k_sample_sectioned(
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    const KeySched64 ks64 = sched64(seed);
+    const KeySched32 ks32 = sched32(seed);
     for (u64 sj = blockIdx.x; sj < count; sj += gridDim.x) {
         const u64 j = first + sj;
         const i64 mj = counts[j];
@@ -175,6 +253,8 @@ __global__ void __launch_bounds__(1024) k_sample_sectioned(
         const u64 lo = j * S;
         const u64 hi = lo + S < n ? lo + S : n;
         const i64 span = (i64)(hi - lo);
+        const bool pow2 = span >= 2 && (span & (span - 1)) == 0;
+        const int b = pow2 ? __ffsll(span) - 1 : 0;
         const RowT *src = rows + lo;
         if (STAGE) {
             const u32 bytes = (u32)(span * sizeof(RowT));
@@ -196,19 +276,15 @@ __global__ void __launch_bounds__(1024) k_sample_sectioned(
         const u64 um = (u64)mj;
         if (MODE == AK_RNG_REFERENCE) {
             constexpr int U = 2;
-            for (u64 b = 0; b < um; b += (u64)blockDim.x * U) {
+            for (u64 bb = 0; bb < um; bb += (u64)blockDim.x * U) {
+                u64 wd[U];
+#pragma unroll
+                for (int t = 0; t < U; ++t)
+                    wd[t] = philox64_sched(ctr0 + bb + (u64)t * blockDim.x + threadIdx.x, strm, ks64);
 #pragma unroll
                 for (int t = 0; t < U; ++t) {
-                    u64 i = b + (u64)t * blockDim.x + threadIdx.x;
-                    if (i < um) {
-                        double uu = ak_uniform_ref(ctr0 + i, strm, seed);
-                        double x = uu * (double)span;
-                        i64 k = (i64)x;
-                        if (k >= span) k = span - 1;
-                        RowT r = tab[k];
-                        o[i] = ((x - (double)k) * avg < (double)r.tw) ? (i64)(lo + k + 1)
-                                                                       : (i64)r.alias;
-                    }
+                    const u64 i = bb + (u64)t * blockDim.x + threadIdx.x;
+                    if (i < um) o[i] = rule_word(tab, wd[t], span, b, pow2, (i64)lo, avg);
                 }
             }
         } else {
@@ -217,22 +293,11 @@ __global__ void __launch_bounds__(1024) k_sample_sectioned(
             const u64 off = ctr0 & 1;
             const u64 npairs = (um + off + 1) / 2;
             for (u64 p = threadIdx.x; p < npairs; p += blockDim.x) {
-                double u0, u1;
-                ph4_pair((ctr0 >> 1) + p, strm, seed, u0, u1);
-                i64 i0 = (i64)(2 * p) - (i64)off;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    i64 i = i0 + h;
-                    if (i >= 0 && (u64)i < um) {
-                        double uu = h ? u1 : u0;
-                        double x = uu * (double)span;
-                        i64 k = (i64)x;
-                        if (k >= span) k = span - 1;
-                        RowT r = tab[k];
-                        o[i] = ((x - (double)k) * avg < (double)r.tw) ? (i64)(lo + k + 1)
-                                                                       : (i64)r.alias;
-                    }
-                }
+                u64 w0, w1;
+                philox32_sched((ctr0 >> 1) + p, strm, ks32, w0, w1);
+                const i64 i0 = (i64)(2 * p) - (i64)off;
+                if (i0 >= 0 && (u64)i0 < um) o[i0] = rule_word(tab, w0, span, b, pow2, (i64)lo, avg);
+                if ((u64)(i0 + 1) < um) o[i0 + 1] = rule_word(tab, w1, span, b, pow2, (i64)lo, avg);
             }
         }
         if (STAGE) __syncthreads();  // rows buffer reused by the next section

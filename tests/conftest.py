@@ -89,3 +89,36 @@ def random_weights(rng, n, kind):
 
 def golden_cases(golden):
     return list(range(len(golden["sizes"])))
+
+
+def near_tie_margins(w, total, rows):
+    """For 1-based rows whose alias differs from the reference, the distance
+    (in units of avg) from the row's key to the nearest key of the other
+    class, with every prefix summed exactly (math.fsum).  A decision taken
+    inside the reference's own rounding noise (a near-tie) has a margin of
+    ~1e-13; a real disagreement has a margin of order 1."""
+    import math
+
+    w = np.asarray(w, dtype=np.float64)
+    n = w.size
+    avg = total / n
+    light = w <= avg
+    li = np.nonzero(light)[0]
+    hi = np.nonzero(~light)[0]
+    # exact prefix keys, correctly rounded
+    dl = [math.fsum([avg] * k + [-x for x in w[li[:k]]]) for k in range(len(li) + 1)]
+    dh = [math.fsum([x for x in w[hi[: j + 1]]] + [-avg] * (j + 1)) for j in range(len(hi))]
+    dl_arr, dh_arr = np.array(dl[:-1]), np.array(dh)
+    pos_l = {int(i): k for k, i in enumerate(li)}
+    pos_h = {int(i): j for j, i in enumerate(hi)}
+    out = []
+    for r in rows:
+        i = int(r) - 1
+        if i in pos_l:
+            x = dl_arr[pos_l[i]]
+            m = float(np.min(np.abs(dh_arr - x))) if dh_arr.size else math.inf
+        else:
+            y = dh_arr[pos_h[i]]
+            m = float(np.min(np.abs(dl_arr - y))) if dl_arr.size else math.inf
+        out.append(m / avg)
+    return out

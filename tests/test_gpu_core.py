@@ -20,15 +20,17 @@ DEV = "cuda"
 
 def test_philox_kats_on_device(hand):
     kats = hand["philox2x64_10_kat"]
-    ctr = torch.tensor([int(k["ctr"][0], 16) for k in kats], dtype=torch.uint64, device=DEV)
-    strm = torch.tensor([int(k["ctr"][1], 16) for k in kats], dtype=torch.uint64, device=DEV)
-    key = torch.tensor([int(k["key"], 16) for k in kats], dtype=torch.uint64, device=DEV)
-    w0 = torch.empty(3, dtype=torch.uint64, device=DEV)
-    w1 = torch.empty(3, dtype=torch.uint64, device=DEV)
+    s64 = lambda x: x - (1 << 64) if x >= (1 << 63) else x
+    col = lambda vals: torch.tensor([s64(v) for v in vals], dtype=torch.int64, device=DEV)
+    ctr = col([int(k["ctr"][0], 16) for k in kats])
+    strm = col([int(k["ctr"][1], 16) for k in kats])
+    key = col([int(k["key"], 16) for k in kats])
+    w0 = torch.empty(3, dtype=torch.int64, device=DEV)
+    w1 = torch.empty(3, dtype=torch.int64, device=DEV)
     _lib.check(_lib.lib().ak_philox2x64(ctr.data_ptr(), strm.data_ptr(), key.data_ptr(), 3,
                                         w0.data_ptr(), w1.data_ptr(), _lib.stream_ptr()))
-    got0 = [int(x) & (2**64 - 1) for x in w0.cpu().view(torch.int64).tolist()]
-    got1 = [int(x) & (2**64 - 1) for x in w1.cpu().view(torch.int64).tolist()]
+    got0 = [x & (2**64 - 1) for x in w0.cpu().tolist()]
+    got1 = [x & (2**64 - 1) for x in w1.cpu().tolist()]
     assert got0 == [int(k["w0"], 16) for k in kats]
     assert got1 == [int(x, 16) for x in hand["philox2x64_10_kat_w1_random123"]]
 
