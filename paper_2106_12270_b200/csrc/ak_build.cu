@@ -34,12 +34,13 @@
 //                    the first heavy tile covering its light keys (T1) and
 //                    the first light tile covering its heavy keys (S1), and
 //                    the first heavy after it (nextH).
-//  3. k_build_pack   warp per 256-item chunk, no block barriers: rebuild the
-//                    chunk's keys, resolve its lights against the heavy
-//                    chunks whose key ranges cover them and its heavies
-//                    against the covering light chunks (L2-resident: the
-//                    neighbouring warps own them), stage the 256 rows in
-//                    shared memory and store them once, coalesced.
+//  3. k_build_pack   CTA per tile: rebuild the tile's keys (lights and heavies
+//                    key-sorted in shared memory), find each element's target
+//                    chunk of the other class, group equal targets, and let
+//                    each warp rebuild one target chunk's keys and resolve its
+//                    group (foreign chunks are L2-resident: neighbouring CTAs
+//                    own them); stage the 2048 rows in shared memory and
+//                    store them once, coalesced.
 //  DRAM traffic ~ read w twice + write the rows once = the algorithmic bytes.
 #include "ak_common.cuh"
 
@@ -191,8 +192,28 @@ __device__ __forceinline__ void lane_class(const double v[VV], double avg, doubl
     double inc = warp_scan_mono(s, lane);
     excl = shfl_up_d(inc, 1);
     if (lane == 0) excl = 0.0;
-    total = shfl_idx_d(inc, 31);
+    total = inc;  // unused by callers that take bounds from pass 1
     mask = m;
+}
+
+// Lane sums of one class and the canonical chunk total: a butterfly (xor)
+// tree sum, identical in every lane and every kernel.
+template <bool LIGHT>
+__device__ __forceinline__ double chunk_total(const double v[VV], double avg, u32 &mask)
+{
+    double s = 0.0;
+    u32 m = 0;
+#pragma unroll
+    for (int k = 0; k < VV; ++k) {
+        const bool valid = v[k] >= 0.0;
+        const bool in = LIGHT ? (valid && v[k] <= avg) : (valid && v[k] > avg);
+        if (in) s = s + (LIGHT ? (avg - v[k]) : (v[k] - avg));
+        m |= (u32)in << k;
+    }
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) s = s + __shfl_xor_sync(0xffffffffu, s, d);
+    mask = m;
+    return s;
 }
 
 // Canonical keys of one class given the chunk's [base, bound].
@@ -252,10 +273,9 @@ __global__ void __launch_bounds__(TB) k_build_scan(const T *__restrict__ w, u64 
 #pragma unroll
         for (int k = 0; k < VV; ++k) v[k] = vnext[k];
         if (j + 1 < tn) load8(w, n, (t + 1) * TILE + (u64)threadIdx.x * VV, vnext);
-        double loc[VV], ex, totD, totE;
         u32 lm, hm;
-        lane_class<true>(v, avg, loc, lm, ex, totD, lane);
-        lane_class<false>(v, avg, loc, hm, ex, totE, lane);
+        const double totD = chunk_total<true>(v, avg, lm);
+        const double totE = chunk_total<false>(v, avg, hm);
         u32 nl = __popc(lm);
 #pragma unroll
         for (int d = 16; d >= 1; d >>= 1) nl += __shfl_xor_sync(0xffffffffu, nl, d);
@@ -453,14 +473,34 @@ __global__ void k_build_coarse(BuildWs W, u64 n)
 }
 
 // ---------------------------------------------------------------------------
-// 3. warp-per-chunk pack
+// 3. target-driven tile pack
 // ---------------------------------------------------------------------------
-template <typename T> struct WarpSmem {
-    double K[CH];   // own keys: lights [0, nL), heavies [nL, nL + nH)
-    double F[CH];   // keys of one class of one foreign chunk
-    typename RowOf<T>::type R[CH];
-    unsigned char P[CH];
-    unsigned char FP[CH];
+// One CTA owns one tile (8 warps).  (a) The warps rebuild the canonical keys
+// of the tile and lay out its lights and heavies key-sorted in shared memory.
+// (b) For each class, every own element gets its target: the foreign chunk
+// (of the other class) holding the first key past it — found among the <= 4
+// candidate tiles whose own-frame chunk bounds sit in shared memory, or by a
+// search over the global tile bases when the candidate range is wide (a tile
+// holding a giant heavy).  (c) Elements are key-sorted, so equal targets form
+// contiguous groups; each warp takes a group, rebuilds the keys of that one
+// foreign chunk and resolves the group's elements there.  (d) The tile's rows
+// are stored once, coalesced.  Each foreign chunk is scanned once per tile.
+constexpr int MAXSLOT = 4;       // candidate foreign tiles handled in shared memory
+constexpr int GCAP = 256;        // groups per round
+constexpr u32 TG_NONE = 0xFFFFFFFFu;
+
+template <typename T> struct PackSmem {
+    double OK[TILE];                    // own keys: lights [0,nL), heavies [nL,nL+nH)
+    typename RowOf<T>::type RW[TILE];   // staged rows
+    u32 TG[TILE];                       // target chunk (tile*8+c) per own element
+    unsigned short OP[TILE];            // own item offsets
+    double F[NW][CH];                   // per-warp foreign chunk keys
+    unsigned char FP[NW][CH];           // per-warp foreign item offsets
+    dd SB[MAXSLOT * NW + 1];            // own-frame chunk bounds of the candidate tiles
+    unsigned short GS[GCAP + 1];        // group starts
+    u32 GT[GCAP];                       // group targets
+    u32 cntL[NW], cntH[NW];
+    u32 ngroups, nslots, done;
 };
 
 // d + x as a normalised double-double (exact for the key ranges in play)
@@ -477,233 +517,327 @@ __device__ __forceinline__ dd add_dd_d(dd d, double x)
 __device__ __forceinline__ bool le_d_dd(double f, dd X) { return f < X.hi || (f == X.hi && X.lo >= 0.0); }
 __device__ __forceinline__ bool lt_d_dd(double f, dd X) { return f < X.hi || (f == X.hi && X.lo > 0.0); }
 
-// first heavy item (0-based) after chunk c of tile t, NONE64 if none;
-// fh_lane = mfh[t*8 + lane] on lanes < 8
-__device__ __forceinline__ u64 next_heavy_after(const BuildWs &W, u64 t, int c,
-                                                unsigned char fh_lane, int lane)
+// first heavy item (0-based) after chunk c of tile t (NONE64 if none)
+__device__ __forceinline__ u64 next_heavy_after(const BuildWs &W, u64 t, int c, int lane)
 {
-    unsigned m = __ballot_sync(0xffffffffu, lane < NW && lane > c && fh_lane != NOFH);
+    const unsigned char fh = lane < NW ? W.mfh[t * NW + lane] : NOFH;
+    unsigned m = __ballot_sync(0xffffffffu, lane < NW && lane > c && fh != NOFH);
     if (m) {
         int cc = __ffs(m) - 1;
-        unsigned char f = (unsigned char)__shfl_sync(0xffffffffu, (int)fh_lane, cc);
+        unsigned char f = (unsigned char)__shfl_sync(0xffffffffu, (int)fh, cc);
         return t * TILE + (u64)cc * CH + f;
     }
     return W.nextH[t];
 }
 
-// compact one class of foreign chunk (tile t, chunk c) into S.F / S.FP
+// Canonical keys of one class of foreign chunk (t, c), compacted into F/FP.
 template <typename T, bool LIGHT>
-__device__ __forceinline__ u32 foreign_chunk(const T *__restrict__ w, u64 n, double avg, u64 fb,
-                                             double base, double bound, WarpSmem<T> &S, int lane)
+__device__ __forceinline__ u32 scan_foreign(const T *__restrict__ w, u64 n, double avg,
+                                            const BuildWs &W, u64 t, int c, double *F,
+                                            unsigned char *FP, int lane)
 {
-    double fv[VV], fk[VV], fex, ftot;
-    u32 fm;
-    load8(w, n, fb + (u64)lane * VV, fv);
-    lane_class<LIGHT>(fv, avg, fk, fm, fex, ftot, lane);
-    class_keys(fk, fex, base, bound, lane);
-    const u32 fc = __popc(fm);
-    u32 fi = fc;
+    const double *mB = LIGHT ? W.mD : W.mE;
+    const double base = c ? mB[t * NW + c - 1] : 0.0, bound = mB[t * NW + c];
+    double v[VV], k[VV], ex, tot;
+    u32 m;
+    load8(w, n, t * TILE + (u64)c * CH + (u64)lane * VV, v);
+    lane_class<LIGHT>(v, avg, k, m, ex, tot, lane);
+    class_keys(k, ex, base, bound, lane);
+    const u32 cnt = __popc(m);
+    u32 inc = cnt;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-        u32 a = __shfl_up_sync(0xffffffffu, fi, d);
-        if (lane >= d) fi += a;
+        u32 a = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += a;
     }
-    const u32 nF = __shfl_sync(0xffffffffu, fi, 31);
+    const u32 nF = __shfl_sync(0xffffffffu, inc, 31);
     __syncwarp();
-    u32 rr = fi - fc;
+    u32 r = inc - cnt;
 #pragma unroll
-    for (int k = 0; k < VV; ++k)
-        if ((fm >> k) & 1) {
-            S.F[rr] = fk[k];
-            if (!LIGHT) S.FP[rr] = (unsigned char)(lane * VV + k);
-            ++rr;
+    for (int q = 0; q < VV; ++q)
+        if ((m >> q) & 1) {
+            F[r] = k[q];
+            FP[r] = (unsigned char)(lane * VV + q);
+            ++r;
         }
     __syncwarp();
     return nF;
 }
 
+// Resolve one class of the own tile.  ISL: own lights against foreign heavy
+// chunks (alias); else own heavies against foreign light chunks (threshold).
+template <typename T, bool ISL>
+__device__ void resolve_class(const T *__restrict__ w, u64 n, double avg, const BuildWs &W,
+                              PackSmem<T> &P, u64 u, u64 tb, u32 ob, u32 cnt)
+{
+    typedef typename RowOf<T>::type RowT;
+    typedef decltype(RowT::alias) AliasT;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const u64 nt = W.nt;
+    const dd DLu = W.DLb[u], DHu = W.DHb[u];
+    const u64 fT0 = ISL ? W.T1[u] : W.S1[u];
+    const u64 fT1 = ISL ? W.T1[u + 1] : W.S1[u + 1];
+    // own frame: foreign key F (rel t) compares with own key x as F vs x + D_t
+    auto Dt = [&](u64 t) -> dd { return ISL ? dd_sub(DLu, W.DHb[t]) : dd_sub(DHu, W.DLb[t]); };
+    const bool fast = fT1 - fT0 + 1 <= (u64)MAXSLOT;
+    const u32 nslot = fast ? (u32)(fT1 - fT0 + 1) : 0;
+    if (fast) {
+        // own-frame bounds: element x targets the first (s,c) with
+        //   ISL:  x + D < mE[c]  <=>  x < mE[c] - D
+        //   !ISL: x + D <= mD[c] <=>  x <= mD[c] - D
+        for (u32 i = threadIdx.x; i < nslot * NW; i += TB) {
+            const u64 t = fT0 + i / NW;
+            if (t >= nt) {
+                P.SB[i] = dd_make(INFINITY, 0.0);
+            } else {
+                const double b = (ISL ? W.mE : W.mD)[t * NW + i % NW];
+                const dd D = Dt(t);
+                P.SB[i] = add_dd_d(dd_neg(D), b);
+            }
+        }
+    }
+    __syncthreads();
+    // (b) targets
+    for (u32 i = threadIdx.x; i < cnt; i += TB) {
+        const double x = P.OK[ob + i];
+        u32 tg = TG_NONE;
+        if (fast) {
+            u32 a = 0, b = nslot * NW;  // first bound passing x
+            while (a < b) {
+                u32 mid = (a + b) >> 1;
+                const bool before = ISL ? !lt_d_dd(x, P.SB[mid]) : !le_d_dd(x, P.SB[mid]);
+                if (before) a = mid + 1;
+                else b = mid;
+            }
+            if (a < nslot * NW) {
+                const u64 t = fT0 + a / NW;
+                tg = t < nt ? (u32)(t * NW + a % NW) : TG_NONE;
+            }
+        } else {
+            // tile: first t in [fT0, fT1] with x + D_t < (<=) tile total, i.e.
+            //   ISL: DLu + x < DHb[t+1];  !ISL: DHu + x <= DLb[t+1]
+            u64 a = fT0, b = fT1 + 1;
+            while (a < b) {
+                const u64 mid = (a + b) >> 1;
+                bool before;
+                if (mid >= nt) before = false;
+                else {
+                    const dd L = ISL ? dd_sub(W.DHb[mid + 1], DLu) : dd_sub(W.DLb[mid + 1], DHu);
+                    before = ISL ? !lt_d_dd(x, L) : !le_d_dd(x, L);
+                }
+                if (before) a = mid + 1;
+                else b = mid;
+            }
+            if (a <= fT1 && a < nt) {
+                const dd D = Dt(a);
+                const double *mB = (ISL ? W.mE : W.mD) + a * NW;
+                int c = 0;
+                for (; c < NW - 1; ++c) {
+                    const dd B = add_dd_d(dd_neg(D), mB[c]);
+                    if (ISL ? lt_d_dd(x, B) : le_d_dd(x, B)) break;
+                }
+                tg = (u32)(a * NW + c);
+            }
+        }
+        P.TG[i] = tg;
+    }
+    __syncthreads();
+    // (c) groups, in rounds of GCAP
+    u32 e0 = 0;
+    while (e0 < cnt) {
+        // group starts among elements [e0, cnt): thread handles a contiguous run
+        const u32 per = (cnt - e0 + TB - 1) / TB;
+        const u32 i0 = e0 + threadIdx.x * per, i1 = min(i0 + per, cnt);
+        u32 nst = 0;
+        for (u32 i = i0; i < i1; ++i) nst += (i == e0 || P.TG[i] != P.TG[i - 1]);
+        // block exclusive scan of nst
+        u32 inc = nst;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            u32 a = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += a;
+        }
+        if (lane == 31) P.cntL[wid] = inc;
+        __syncthreads();
+        u32 wbase = 0, tot = 0;
+        for (int k = 0; k < NW; ++k) {
+            wbase += k < wid ? P.cntL[k] : 0;
+            tot += P.cntL[k];
+        }
+        u32 g = wbase + inc - nst;
+        for (u32 i = i0; i < i1; ++i)
+            if (i == e0 || P.TG[i] != P.TG[i - 1]) {
+                if (g < GCAP) {
+                    P.GS[g] = (unsigned short)i;
+                    P.GT[g] = P.TG[i];
+                }
+                ++g;
+            }
+        __syncthreads();
+        // when capped, the last recorded group is deferred to the next round
+        const u32 ngr = tot <= GCAP ? tot : GCAP - 1;
+        const u32 e1 = tot <= GCAP ? cnt : P.GS[GCAP - 1];
+        __syncthreads();
+        if (threadIdx.x == 0) P.GS[ngr] = (unsigned short)e1;
+        __syncthreads();
+        for (u32 gi = wid; gi < ngr; gi += NW) {
+            const u32 ga = P.GS[gi], gb = P.GS[gi + 1];
+            const u32 tgt = P.GT[gi];
+            if (tgt == TG_NONE) {
+                if (ISL) {  // no heavy key past these lights: own rows
+                    for (u32 r = ga + lane; r < gb; r += 32) {
+                        const u32 pos = P.OP[ob + r];
+                        P.RW[pos].alias = (AliasT)(tb + pos + 1);
+                    }
+                } else {  // no light key at or past these heavies: DL = total deficit
+                    const dd A = dd_sub(DHu, W.DLb[nt]);
+                    for (u32 r = ga + lane; r < gb; r += 32) {
+                        const dd tw = dd_add_d(add_dd_d(A, P.OK[ob + r]), avg);
+                        P.RW[P.OP[ob + r]].tw = tw_store<T>(tw.hi + tw.lo, avg);
+                    }
+                }
+                continue;
+            }
+            const u64 t = tgt / NW;
+            const int c = (int)(tgt % NW);
+            double *F = P.F[wid];
+            unsigned char *FP = P.FP[wid];
+            const u32 nF = scan_foreign<T, !ISL>(w, n, avg, W, t, c, F, FP, lane);
+            const dd D = Dt(t);
+            if (ISL) {
+                const u64 after = next_heavy_after(W, t, c, lane);
+                const u64 fb = t * TILE + (u64)c * CH;
+                for (u32 r = ga + lane; r < gb; r += 32) {
+                    const dd X = add_dd_d(D, P.OK[ob + r]);
+                    u32 a = 0, b = nF;  // first heavy key > X
+                    while (a < b) {
+                        u32 mid = (a + b) >> 1;
+                        if (le_d_dd(F[mid], X)) a = mid + 1;
+                        else b = mid;
+                    }
+                    const u32 pos = P.OP[ob + r];
+                    u64 al;
+                    if (a < nF) al = fb + FP[a] + 1;
+                    else al = (after == NONE64) ? tb + pos + 1 : after + 1;
+                    P.RW[pos].alias = (AliasT)al;
+                }
+            } else {
+                const double bound = W.mD[t * NW + c];
+                for (u32 r = ga + lane; r < gb; r += 32) {
+                    const dd Y = add_dd_d(D, P.OK[ob + r]);
+                    u32 a = 0, b = nF;  // first light key >= Y
+                    while (a < b) {
+                        u32 mid = (a + b) >> 1;
+                        if (lt_d_dd(F[mid], Y)) a = mid + 1;
+                        else b = mid;
+                    }
+                    const double DL = a < nF ? F[a] : bound;
+                    const dd tw = dd_add_d(add_dd_d(Y, -DL), avg);
+                    P.RW[P.OP[ob + r]].tw = tw_store<T>(tw.hi + tw.lo, avg);
+                }
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        e0 = tot <= GCAP ? cnt : e1;
+    }
+}
+
 template <typename T>
-__global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u64 n, double avg,
+__global__ void __launch_bounds__(TB, 3) k_build_pack(const T *__restrict__ w, u64 n, double avg,
                                                       BuildWs W,
                                                       typename RowOf<T>::type *__restrict__ rows_out)
 {
     typedef typename RowOf<T>::type RowT;
     typedef decltype(RowT::alias) AliasT;
     extern __shared__ __align__(16) unsigned char pack_smem[];
+    PackSmem<T> &P = *reinterpret_cast<PackSmem<T> *>(pack_smem);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    WarpSmem<T> &S = reinterpret_cast<WarpSmem<T> *>(pack_smem)[wid];
-    const u64 nt = W.nt;
     const u64 u = blockIdx.x;
-    const u64 cbase = u * TILE + (u64)wid * CH;  // first item of this chunk
-    if (cbase >= n) return;
+    const u64 tb = u * TILE;
+    const u64 cbase = tb + (u64)wid * CH;
 
-    // ---- own chunk: canonical keys of both classes
+    // (a) own tile: classify, counts, then canonical keys into sorted lists
     double v[VV];
     load8(w, n, cbase + (u64)lane * VV, v);
-    const double bD0 = wid ? W.mD[u * NW + wid - 1] : 0.0, bD1 = W.mD[u * NW + wid];
-    const double bE0 = wid ? W.mE[u * NW + wid - 1] : 0.0, bE1 = W.mE[u * NW + wid];
-    const unsigned char fh_own = lane < NW ? W.mfh[u * NW + lane] : NOFH;
-    const dd DLu = W.DLb[u], DHu = W.DHb[u];
-    u32 lm, hm, nL, nH;
-    {
-        double kD[VV], kE[VV], exD, exE, tD, tE;
-        lane_class<true>(v, avg, kD, lm, exD, tD, lane);
-        lane_class<false>(v, avg, kE, hm, exE, tE, lane);
-        class_keys(kD, exD, bD0, bD1, lane);
-        class_keys(kE, exE, bE0, bE1, lane);
-        const u32 cl = __popc(lm), chh = __popc(hm);
-        u32 il = cl, ih = chh;
+    u32 lm = 0, hm = 0;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            u32 a = __shfl_up_sync(0xffffffffu, il, d), b = __shfl_up_sync(0xffffffffu, ih, d);
-            if (lane >= d) { il += a; ih += b; }
-        }
-        nL = __shfl_sync(0xffffffffu, il, 31);
-        nH = __shfl_sync(0xffffffffu, ih, 31);
-        u32 rl = il - cl, rh = nL + ih - chh;
+    for (int k = 0; k < VV; ++k) {
+        lm |= (u32)(v[k] >= 0.0 && v[k] <= avg) << k;
+        hm |= (u32)(v[k] > avg) << k;
+    }
+    u32 il = __popc(lm), ih = __popc(hm);
+    const u32 cl = il, chh = ih;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        u32 a = __shfl_up_sync(0xffffffffu, il, d), b = __shfl_up_sync(0xffffffffu, ih, d);
+        if (lane >= d) { il += a; ih += b; }
+    }
+    if (lane == 31) {
+        P.cntL[wid] = il;
+        P.cntH[wid] = ih;
+    }
+    __syncthreads();
+    u32 offL = 0, offH = 0, nL = 0, nH = 0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+        offL += k < wid ? P.cntL[k] : 0;
+        offH += k < wid ? P.cntH[k] : 0;
+        nL += P.cntL[k];
+        nH += P.cntH[k];
+    }
+    {
+        const double bD0 = wid ? W.mD[u * NW + wid - 1] : 0.0, bD1 = W.mD[u * NW + wid];
+        const double bE0 = wid ? W.mE[u * NW + wid - 1] : 0.0, bE1 = W.mE[u * NW + wid];
+        double kD[VV], kE[VV], exD, exE, tD, tE;
+        u32 m1, m2;
+        lane_class<true>(v, avg, kD, m1, exD, tD, lane);
+        class_keys(kD, exD, bD0, bD1, lane);
+        lane_class<false>(v, avg, kE, m2, exE, tE, lane);
+        class_keys(kE, exE, bE0, bE1, lane);
+        u32 rl = offL + il - cl, rh = nL + offH + ih - chh;
 #pragma unroll
         for (int k = 0; k < VV; ++k) {
-            const u32 pos = lane * VV + k;
+            const u32 pos = wid * CH + lane * VV + k;
             if ((lm >> k) & 1) {
-                S.K[rl] = kD[k];
-                S.P[rl] = (unsigned char)pos;
-                S.R[pos].tw = (decltype(RowT::tw))v[k];
+                P.OK[rl] = kD[k];
+                P.OP[rl] = (unsigned short)pos;
+                P.RW[pos].tw = (decltype(RowT::tw))v[k];
                 ++rl;
             } else if ((hm >> k) & 1) {
-                S.K[rh] = kE[k];
-                S.P[rh] = (unsigned char)pos;
+                P.OK[rh] = kE[k];
+                P.OP[rh] = (unsigned short)pos;
                 ++rh;
             }
         }
     }
-    __syncwarp();
-    // heavy aliases: next heavy in the chunk, else after the chunk
+    __syncthreads();
+    // heavy aliases: the next heavy of the tile, else the first heavy after it
     {
-        const u64 after = next_heavy_after(W, u, wid, fh_own, lane);
-        for (u32 r = lane; r < nH; r += 32) {
-            const u32 pos = S.P[nL + r];
+        const u64 after = W.nextH[u];
+        for (u32 r = threadIdx.x; r < nH; r += TB) {
+            const u32 pos = P.OP[nL + r];
             u64 a;
-            if (r + 1 < nH) a = cbase + S.P[nL + r + 1] + 1;
-            else a = (after == NONE64) ? cbase + pos + 1 : after + 1;
-            S.R[pos].alias = (AliasT)a;
+            if (r + 1 < nH) a = tb + P.OP[nL + r + 1] + 1;
+            else a = (after == NONE64) ? tb + pos + 1 : after + 1;
+            P.RW[pos].alias = (AliasT)a;
         }
     }
-
-    // ---- lights: alias = first heavy (in key order) with key > light key
-    if (nL) {
-        u32 r0 = 0;
-        const u64 tA = W.T1[u], tB = W.T1[u + 1];
-        for (u64 t = tA; t <= tB && r0 < nL; ++t) {
-            if (t >= nt) {
-                for (u32 r = r0 + lane; r < nL; r += 32) {
-                    const u32 pos = S.P[r];
-                    S.R[pos].alias = (AliasT)(cbase + pos + 1);
-                }
-                r0 = nL;
-                break;
-            }
-            const dd Dl = dd_sub(DLu, W.DHb[t]);  // heavy (rel t) <= light (rel u): hk <= lk + Dl
-            const double mE_l = lane < NW ? W.mE[t * NW + lane] : 0.0;
-            const unsigned char fh_l = lane < NW ? W.mfh[t * NW + lane] : NOFH;
-            for (int c = 0; c < NW && r0 < nL; ++c) {
-                const double bnd = __shfl_sync(0xffffffffu, mE_l, c);
-                // lights resolved by chunk c: lk + Dl < bnd
-                u32 lo = r0, hi = nL;
-                while (lo < hi) {
-                    u32 mid = (lo + hi) >> 1;
-                    if (!le_d_dd(bnd, add_dd_d(Dl, S.K[mid]))) lo = mid + 1;
-                    else hi = mid;
-                }
-                const u32 r1 = lo;
-                if (r1 == r0) continue;
-                const u64 fb = t * TILE + (u64)c * CH;
-                const double b0 = c ? __shfl_sync(0xffffffffu, mE_l, c - 1) : 0.0;
-                const u32 nF = foreign_chunk<T, false>(w, n, avg, fb, b0, bnd, S, lane);
-                const u64 after = next_heavy_after(W, t, c, fh_l, lane);
-                for (u32 r = r0 + lane; r < r1; r += 32) {
-                    const dd X = add_dd_d(Dl, S.K[r]);
-                    u32 a = 0, b = nF;  // first m with F[m] > X
-                    while (a < b) {
-                        u32 mid = (a + b) >> 1;
-                        if (le_d_dd(S.F[mid], X)) a = mid + 1;
-                        else b = mid;
-                    }
-                    const u32 pos = S.P[r];
-                    u64 al;
-                    if (a < nF) al = fb + S.FP[a] + 1;
-                    else al = (after == NONE64) ? cbase + pos + 1 : after + 1;
-                    S.R[pos].alias = (AliasT)al;
-                }
-                __syncwarp();
-                r0 = r1;
-            }
-        }
-        // defensive: lights left over (inconsistent bounds) keep their own row
-        for (u32 r = r0 + lane; r < nL; r += 32) {
-            const u32 pos = S.P[r];
-            S.R[pos].alias = (AliasT)(cbase + pos + 1);
-        }
-    }
-
-    // ---- heavies: tw = key - DL(first light with key >= heavy key) + avg
-    if (nH) {
-        u32 r0 = 0;
-        const u64 sA = W.S1[u], sB = W.S1[u + 1];
-        const double *HK = S.K + nL;
-        const unsigned char *HP = S.P + nL;
-        for (u64 s = sA; s <= sB && r0 < nH; ++s) {
-            if (s >= nt) break;
-            const dd Dh = dd_sub(DHu, W.DLb[s]);  // light (rel s) < heavy (rel u): lk < hk + Dh
-            const double mD_l = lane < NW ? W.mD[s * NW + lane] : 0.0;
-            for (int c = 0; c < NW && r0 < nH; ++c) {
-                const double bnd = __shfl_sync(0xffffffffu, mD_l, c);
-                // heavies resolved by chunk c: hk + Dh <= bnd
-                u32 lo = r0, hi = nH;
-                while (lo < hi) {
-                    u32 mid = (lo + hi) >> 1;
-                    if (!lt_d_dd(bnd, add_dd_d(Dh, HK[mid]))) lo = mid + 1;
-                    else hi = mid;
-                }
-                const u32 r1 = lo;
-                if (r1 == r0) continue;
-                const u64 fb = s * TILE + (u64)c * CH;
-                const double b0 = c ? __shfl_sync(0xffffffffu, mD_l, c - 1) : 0.0;
-                const u32 nF = foreign_chunk<T, true>(w, n, avg, fb, b0, bnd, S, lane);
-                for (u32 r = r0 + lane; r < r1; r += 32) {
-                    const dd Y = add_dd_d(Dh, HK[r]);
-                    u32 a = 0, b = nF;  // first m with F[m] >= Y
-                    while (a < b) {
-                        u32 mid = (a + b) >> 1;
-                        if (lt_d_dd(S.F[mid], Y)) a = mid + 1;
-                        else b = mid;
-                    }
-                    const double DL = a < nF ? S.F[a] : bnd;  // rel s
-                    // tw = (DHu + hk) - (DLb[s] + DL) + avg = Y - DL + avg
-                    const dd tw = dd_add_d(add_dd_d(Y, -DL), avg);
-                    S.R[HP[r]].tw = tw_store<T>(tw.hi + tw.lo, avg);
-                }
-                __syncwarp();
-                r0 = r1;
-            }
-        }
-        // heavies above every light key: DL = the total deficit
-        const dd A = dd_sub(DHu, W.DLb[nt]);
-        for (u32 r = r0 + lane; r < nH; r += 32) {
-            const dd tw = dd_add_d(add_dd_d(A, HK[r]), avg);
-            S.R[HP[r]].tw = tw_store<T>(tw.hi + tw.lo, avg);
-        }
-    }
-    __syncwarp();
-    // ---- store the chunk's rows (each lane its 8 consecutive rows)
+    // (b, c) resolve lights, then heavies
+    if (nL) resolve_class<T, true>(w, n, avg, W, P, u, tb, 0, nL);
+    if (nH) resolve_class<T, false>(w, n, avg, W, P, u, tb, nL, nH);
+    __syncthreads();
+    // (d) store the tile's rows: each lane its 8 consecutive rows
     const u64 i0 = cbase + (u64)lane * VV;
+    const u32 p0 = wid * CH + lane * VV;
     if (i0 + VV <= n) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(&S.R[lane * VV]);
+        const uint4 *src = reinterpret_cast<const uint4 *>(&P.RW[p0]);
         uint4 *dst = reinterpret_cast<uint4 *>(rows_out + i0);
 #pragma unroll
         for (int q = 0; q < (int)(VV * sizeof(RowT) / 16); ++q) dst[q] = src[q];
     } else {
         for (int k = 0; k < VV; ++k)
-            if (i0 + k < n) rows_out[i0 + k] = S.R[lane * VV + k];
+            if (i0 + k < n) rows_out[i0 + k] = P.RW[p0 + k];
     }
 }
 
@@ -719,7 +853,7 @@ int run_build(const void *wv, u64 n, double total, void *rows, void *ws, cudaStr
     AK_LAUNCH_CHECK("k_build_scan");
     k_build_coarse<<<(unsigned)((W.nt + 1 + 255) / 256), 256, 0, st>>>(W, n);
     AK_LAUNCH_CHECK("k_build_coarse");
-    const size_t smem = sizeof(WarpSmem<T>) * NW;
+    const size_t smem = sizeof(PackSmem<T>);
     AK_CUDA_TRY(cudaFuncSetAttribute(k_build_pack<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
     k_build_pack<T><<<(unsigned)W.nt, TB, smem, st>>>(w, n, avg, W, (typename RowOf<T>::type *)rows);
