@@ -34,13 +34,12 @@
 //                    the first heavy tile covering its light keys (T1) and
 //                    the first light tile covering its heavy keys (S1), and
 //                    the first heavy after it (nextH).
-//  3. k_build_pack   CTA per tile: rebuild the tile's keys (lights and heavies
-//                    key-sorted in shared memory), find each element's target
-//                    chunk of the other class, group equal targets, and let
-//                    each warp rebuild one target chunk's keys and resolve its
-//                    group (foreign chunks are L2-resident: neighbouring CTAs
-//                    own them); stage the 2048 rows in shared memory and
-//                    store them once, coalesced.
+//  3. k_build_pack   persistent warps stream through runs of chunks taken in
+//                    order from a global queue, resolving each own chunk
+//                    against two sliding windows of foreign keys (the heavies
+//                    after its lights, the lights at or after its heavies),
+//                    advanced chunk by chunk; rows staged in shared memory
+//                    and stored once, coalesced.
 //  DRAM traffic ~ read w twice + write the rows once = the algorithmic bytes.
 #include "ak_common.cuh"
 
@@ -473,34 +472,30 @@ __global__ void k_build_coarse(BuildWs W, u64 n)
 }
 
 // ---------------------------------------------------------------------------
-// 3. target-driven tile pack
+// 3. warp-streaming pack
 // ---------------------------------------------------------------------------
-// One CTA owns one tile (8 warps).  (a) The warps rebuild the canonical keys
-// of the tile and lay out its lights and heavies key-sorted in shared memory.
-// (b) For each class, every own element gets its target: the foreign chunk
-// (of the other class) holding the first key past it — found among the <= 4
-// candidate tiles whose own-frame chunk bounds sit in shared memory, or by a
-// search over the global tile bases when the candidate range is wide (a tile
-// holding a giant heavy).  (c) Elements are key-sorted, so equal targets form
-// contiguous groups; each warp takes a group, rebuilds the keys of that one
-// foreign chunk and resolves the group's elements there.  (d) The tile's rows
-// are stored once, coalesced.  Each foreign chunk is scanned once per tile.
-constexpr int MAXSLOT = 4;       // candidate foreign tiles handled in shared memory
-constexpr int GCAP = 256;        // groups per round
-constexpr u32 TG_NONE = 0xFFFFFFFFu;
+// Every warp takes runs of RUN consecutive chunks from a global queue (runs
+// are handed out in order, so the runs in flight — and the foreign chunks
+// they read — stay L2-resident) and streams through them.  It keeps two
+// warp-private sliding windows of global double-double keys:
+//   HW: the heavies following its current lights in key order,
+//   LW: the lights at or after its current heavies in key order,
+// each advanced monotonically by rebuilding the canonical keys of the next
+// foreign chunk of that class (chunks whose key range lies entirely behind
+// the request are skipped via the pass-1 chunk bounds).  An own chunk is
+// resolved against the windows and its 256 rows are stored once, coalesced.
+// No block barriers: warps are independent.
+constexpr int RUN = 16;          // chunks per queue item
+constexpr int WCAP = 512;        // window capacity (entries); a chunk adds <= 256
+constexpr int PW = 4;            // warps per CTA
 
-template <typename T> struct PackSmem {
-    double OK[TILE];                    // own keys: lights [0,nL), heavies [nL,nL+nH)
-    typename RowOf<T>::type RW[TILE];   // staged rows
-    u32 TG[TILE];                       // target chunk (tile*8+c) per own element
-    unsigned short OP[TILE];            // own item offsets
-    double F[NW][CH];                   // per-warp foreign chunk keys
-    unsigned char FP[NW][CH];           // per-warp foreign item offsets
-    dd SB[MAXSLOT * NW + 1];            // own-frame chunk bounds of the candidate tiles
-    unsigned short GS[GCAP + 1];        // group starts
-    u32 GT[GCAP];                       // group targets
-    u32 cntL[NW], cntH[NW];
-    u32 ngroups, nslots, done;
+template <typename T> struct WarpSmem {
+    dd OK[CH];                        // own global keys: lights [0,nl), heavies [nl,nl+nh)
+    dd HK[WCAP];                      // heavy window keys (ring)
+    dd LK[WCAP];                      // light window keys (ring)
+    typename RowOf<T>::type RW[CH];   // staged rows
+    u32 HI[WCAP];                     // heavy window items (0-based)
+    unsigned char OP[CH];             // own item offsets
 };
 
 // d + x as a normalised double-double (exact for the key ranges in play)
@@ -513,34 +508,32 @@ __device__ __forceinline__ dd add_dd_d(dd d, double x)
     fast_two_sum(s, e, h, l);
     return dd_make(h, l);
 }
-// f <= X and f < X for normalised X
-__device__ __forceinline__ bool le_d_dd(double f, dd X) { return f < X.hi || (f == X.hi && X.lo >= 0.0); }
-__device__ __forceinline__ bool lt_d_dd(double f, dd X) { return f < X.hi || (f == X.hi && X.lo > 0.0); }
 
-// first heavy item (0-based) after chunk c of tile t (NONE64 if none)
-__device__ __forceinline__ u64 next_heavy_after(const BuildWs &W, u64 t, int c, int lane)
+__device__ __forceinline__ dd chunk_base(const BuildWs &W, u64 g, bool light, bool upper)
 {
-    const unsigned char fh = lane < NW ? W.mfh[t * NW + lane] : NOFH;
-    unsigned m = __ballot_sync(0xffffffffu, lane < NW && lane > c && fh != NOFH);
-    if (m) {
-        int cc = __ffs(m) - 1;
-        unsigned char f = (unsigned char)__shfl_sync(0xffffffffu, (int)fh, cc);
-        return t * TILE + (u64)cc * CH + f;
-    }
-    return W.nextH[t];
+    // global lower (upper) bound of the keys of one class in chunk g
+    const u64 t = g / NW;
+    const int c = (int)(g % NW);
+    const double *mB = light ? W.mD : W.mE;
+    const double loc = upper ? mB[g] : (c ? mB[g - 1] : 0.0);
+    return add_dd_d(light ? W.DLb[t] : W.DHb[t], loc);
 }
 
-// Canonical keys of one class of foreign chunk (t, c), compacted into F/FP.
+// Canonical global keys of one class of chunk g, appended to a window ring.
+// Returns the number appended.
 template <typename T, bool LIGHT>
-__device__ __forceinline__ u32 scan_foreign(const T *__restrict__ w, u64 n, double avg,
-                                            const BuildWs &W, u64 t, int c, double *F,
-                                            unsigned char *FP, int lane)
+__device__ __forceinline__ u32 append_chunk(const T *__restrict__ w, u64 n, double avg,
+                                            const BuildWs &W, u64 g, dd *K, u32 *I, u32 tail,
+                                            int lane)
 {
+    const u64 t = g / NW;
+    const int c = (int)(g % NW);
     const double *mB = LIGHT ? W.mD : W.mE;
-    const double base = c ? mB[t * NW + c - 1] : 0.0, bound = mB[t * NW + c];
+    const double base = c ? mB[g - 1] : 0.0, bound = mB[g];
+    const dd B = LIGHT ? W.DLb[t] : W.DHb[t];
     double v[VV], k[VV], ex, tot;
     u32 m;
-    load8(w, n, t * TILE + (u64)c * CH + (u64)lane * VV, v);
+    load8(w, n, g * CH + (u64)lane * VV, v);
     lane_class<LIGHT>(v, avg, k, m, ex, tot, lane);
     class_keys(k, ex, base, bound, lane);
     const u32 cnt = __popc(m);
@@ -550,294 +543,248 @@ __device__ __forceinline__ u32 scan_foreign(const T *__restrict__ w, u64 n, doub
         u32 a = __shfl_up_sync(0xffffffffu, inc, d);
         if (lane >= d) inc += a;
     }
-    const u32 nF = __shfl_sync(0xffffffffu, inc, 31);
-    __syncwarp();
-    u32 r = inc - cnt;
+    const u32 total = __shfl_sync(0xffffffffu, inc, 31);
+    u32 r = tail + inc - cnt;
 #pragma unroll
     for (int q = 0; q < VV; ++q)
         if ((m >> q) & 1) {
-            F[r] = k[q];
-            FP[r] = (unsigned char)(lane * VV + q);
+            const u32 s = r & (WCAP - 1);
+            K[s] = add_dd_d(B, k[q]);
+            if (!LIGHT) I[s] = (u32)(g * CH + lane * VV + q);
             ++r;
         }
     __syncwarp();
-    return nF;
+    return total;
 }
 
-// Resolve one class of the own tile.  ISL: own lights against foreign heavy
-// chunks (alias); else own heavies against foreign light chunks (threshold).
-template <typename T, bool ISL>
-__device__ void resolve_class(const T *__restrict__ w, u64 n, double avg, const BuildWs &W,
-                              PackSmem<T> &P, u64 u, u64 tb, u32 ob, u32 cnt)
+// first index i in [0, cnt) of the ring (from head) with pred(K[i]) false,
+// pred monotone (true then false); warp-uniform
+template <typename P>
+__device__ __forceinline__ u32 ring_search(const dd *K, u32 head, u32 cnt, P pred)
 {
-    typedef typename RowOf<T>::type RowT;
-    typedef decltype(RowT::alias) AliasT;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const u64 nt = W.nt;
-    const dd DLu = W.DLb[u], DHu = W.DHb[u];
-    const u64 fT0 = ISL ? W.T1[u] : W.S1[u];
-    const u64 fT1 = ISL ? W.T1[u + 1] : W.S1[u + 1];
-    // own frame: foreign key F (rel t) compares with own key x as F vs x + D_t
-    auto Dt = [&](u64 t) -> dd { return ISL ? dd_sub(DLu, W.DHb[t]) : dd_sub(DHu, W.DLb[t]); };
-    const bool fast = fT1 - fT0 + 1 <= (u64)MAXSLOT;
-    const u32 nslot = fast ? (u32)(fT1 - fT0 + 1) : 0;
-    if (fast) {
-        // own-frame bounds: element x targets the first (s,c) with
-        //   ISL:  x + D < mE[c]  <=>  x < mE[c] - D
-        //   !ISL: x + D <= mD[c] <=>  x <= mD[c] - D
-        for (u32 i = threadIdx.x; i < nslot * NW; i += TB) {
-            const u64 t = fT0 + i / NW;
-            if (t >= nt) {
-                P.SB[i] = dd_make(INFINITY, 0.0);
-            } else {
-                const double b = (ISL ? W.mE : W.mD)[t * NW + i % NW];
-                const dd D = Dt(t);
-                P.SB[i] = add_dd_d(dd_neg(D), b);
-            }
-        }
+    u32 a = 0, b = cnt;
+    while (a < b) {
+        const u32 mid = (a + b) >> 1;
+        if (pred(K[(head + mid) & (WCAP - 1)])) a = mid + 1;
+        else b = mid;
     }
-    __syncthreads();
-    // (b) targets
-    for (u32 i = threadIdx.x; i < cnt; i += TB) {
-        const double x = P.OK[ob + i];
-        u32 tg = TG_NONE;
-        if (fast) {
-            u32 a = 0, b = nslot * NW;  // first bound passing x
-            while (a < b) {
-                u32 mid = (a + b) >> 1;
-                const bool before = ISL ? !lt_d_dd(x, P.SB[mid]) : !le_d_dd(x, P.SB[mid]);
-                if (before) a = mid + 1;
-                else b = mid;
-            }
-            if (a < nslot * NW) {
-                const u64 t = fT0 + a / NW;
-                tg = t < nt ? (u32)(t * NW + a % NW) : TG_NONE;
-            }
-        } else {
-            // tile: first t in [fT0, fT1] with x + D_t < (<=) tile total, i.e.
-            //   ISL: DLu + x < DHb[t+1];  !ISL: DHu + x <= DLb[t+1]
-            u64 a = fT0, b = fT1 + 1;
-            while (a < b) {
-                const u64 mid = (a + b) >> 1;
-                bool before;
-                if (mid >= nt) before = false;
-                else {
-                    const dd L = ISL ? dd_sub(W.DHb[mid + 1], DLu) : dd_sub(W.DLb[mid + 1], DHu);
-                    before = ISL ? !lt_d_dd(x, L) : !le_d_dd(x, L);
-                }
-                if (before) a = mid + 1;
-                else b = mid;
-            }
-            if (a <= fT1 && a < nt) {
-                const dd D = Dt(a);
-                const double *mB = (ISL ? W.mE : W.mD) + a * NW;
-                int c = 0;
-                for (; c < NW - 1; ++c) {
-                    const dd B = add_dd_d(dd_neg(D), mB[c]);
-                    if (ISL ? lt_d_dd(x, B) : le_d_dd(x, B)) break;
-                }
-                tg = (u32)(a * NW + c);
-            }
-        }
-        P.TG[i] = tg;
+    return a;
+}
+
+// seek: first chunk g >= from whose class bound passes key x
+// (heavies: bound > x; lights: bound >= x), G if none
+template <bool LIGHT>
+__device__ u64 seek_chunk(const BuildWs &W, u64 from, u64 G, dd x)
+{
+    auto passes = [&](u64 g) {
+        const dd b = chunk_base(W, g, LIGHT, true);
+        return LIGHT ? !dd_lt(b, x) : dd_lt(x, b);
+    };
+    if (from >= G || passes(from)) return from;
+    // gallop, then bisect
+    u64 lo = from, step = 1;  // invariant: !passes(lo)
+    while (lo + step < G && !passes(lo + step)) {
+        lo += step;
+        step <<= 1;
     }
-    __syncthreads();
-    // (c) groups, in rounds of GCAP
-    u32 e0 = 0;
-    while (e0 < cnt) {
-        // group starts among elements [e0, cnt): thread handles a contiguous run
-        const u32 per = (cnt - e0 + TB - 1) / TB;
-        const u32 i0 = e0 + threadIdx.x * per, i1 = min(i0 + per, cnt);
-        u32 nst = 0;
-        for (u32 i = i0; i < i1; ++i) nst += (i == e0 || P.TG[i] != P.TG[i - 1]);
-        // block exclusive scan of nst
-        u32 inc = nst;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            u32 a = __shfl_up_sync(0xffffffffu, inc, d);
-            if (lane >= d) inc += a;
-        }
-        if (lane == 31) P.cntL[wid] = inc;
-        __syncthreads();
-        u32 wbase = 0, tot = 0;
-        for (int k = 0; k < NW; ++k) {
-            wbase += k < wid ? P.cntL[k] : 0;
-            tot += P.cntL[k];
-        }
-        u32 g = wbase + inc - nst;
-        for (u32 i = i0; i < i1; ++i)
-            if (i == e0 || P.TG[i] != P.TG[i - 1]) {
-                if (g < GCAP) {
-                    P.GS[g] = (unsigned short)i;
-                    P.GT[g] = P.TG[i];
-                }
-                ++g;
-            }
-        __syncthreads();
-        // when capped, the last recorded group is deferred to the next round
-        const u32 ngr = tot <= GCAP ? tot : GCAP - 1;
-        const u32 e1 = tot <= GCAP ? cnt : P.GS[GCAP - 1];
-        __syncthreads();
-        if (threadIdx.x == 0) P.GS[ngr] = (unsigned short)e1;
-        __syncthreads();
-        for (u32 gi = wid; gi < ngr; gi += NW) {
-            const u32 ga = P.GS[gi], gb = P.GS[gi + 1];
-            const u32 tgt = P.GT[gi];
-            if (tgt == TG_NONE) {
-                if (ISL) {  // no heavy key past these lights: own rows
-                    for (u32 r = ga + lane; r < gb; r += 32) {
-                        const u32 pos = P.OP[ob + r];
-                        P.RW[pos].alias = (AliasT)(tb + pos + 1);
-                    }
-                } else {  // no light key at or past these heavies: DL = total deficit
-                    const dd A = dd_sub(DHu, W.DLb[nt]);
-                    for (u32 r = ga + lane; r < gb; r += 32) {
-                        const dd tw = dd_add_d(add_dd_d(A, P.OK[ob + r]), avg);
-                        P.RW[P.OP[ob + r]].tw = tw_store<T>(tw.hi + tw.lo, avg);
-                    }
-                }
-                continue;
-            }
-            const u64 t = tgt / NW;
-            const int c = (int)(tgt % NW);
-            double *F = P.F[wid];
-            unsigned char *FP = P.FP[wid];
-            const u32 nF = scan_foreign<T, !ISL>(w, n, avg, W, t, c, F, FP, lane);
-            const dd D = Dt(t);
-            if (ISL) {
-                const u64 after = next_heavy_after(W, t, c, lane);
-                const u64 fb = t * TILE + (u64)c * CH;
-                for (u32 r = ga + lane; r < gb; r += 32) {
-                    const dd X = add_dd_d(D, P.OK[ob + r]);
-                    u32 a = 0, b = nF;  // first heavy key > X
-                    while (a < b) {
-                        u32 mid = (a + b) >> 1;
-                        if (le_d_dd(F[mid], X)) a = mid + 1;
-                        else b = mid;
-                    }
-                    const u32 pos = P.OP[ob + r];
-                    u64 al;
-                    if (a < nF) al = fb + FP[a] + 1;
-                    else al = (after == NONE64) ? tb + pos + 1 : after + 1;
-                    P.RW[pos].alias = (AliasT)al;
-                }
-            } else {
-                const double bound = W.mD[t * NW + c];
-                for (u32 r = ga + lane; r < gb; r += 32) {
-                    const dd Y = add_dd_d(D, P.OK[ob + r]);
-                    u32 a = 0, b = nF;  // first light key >= Y
-                    while (a < b) {
-                        u32 mid = (a + b) >> 1;
-                        if (lt_d_dd(F[mid], Y)) a = mid + 1;
-                        else b = mid;
-                    }
-                    const double DL = a < nF ? F[a] : bound;
-                    const dd tw = dd_add_d(add_dd_d(Y, -DL), avg);
-                    P.RW[P.OP[ob + r]].tw = tw_store<T>(tw.hi + tw.lo, avg);
-                }
-            }
-            __syncwarp();
-        }
-        __syncthreads();
-        e0 = tot <= GCAP ? cnt : e1;
+    u64 hi = lo + step < G ? lo + step : G;  // passes(hi) or hi == G
+    while (hi - lo > 1) {
+        const u64 mid = (lo + hi) >> 1;
+        if (passes(mid)) hi = mid;
+        else lo = mid;
     }
+    return hi;
 }
 
 template <typename T>
-__global__ void __launch_bounds__(TB, 3) k_build_pack(const T *__restrict__ w, u64 n, double avg,
-                                                      BuildWs W,
-                                                      typename RowOf<T>::type *__restrict__ rows_out)
+__global__ void __launch_bounds__(PW * 32) k_build_pack(const T *__restrict__ w, u64 n,
+                                                        double avg, BuildWs W,
+                                                        typename RowOf<T>::type *__restrict__ rows_out,
+                                                        unsigned int *queue)
 {
     typedef typename RowOf<T>::type RowT;
     typedef decltype(RowT::alias) AliasT;
     extern __shared__ __align__(16) unsigned char pack_smem[];
-    PackSmem<T> &P = *reinterpret_cast<PackSmem<T> *>(pack_smem);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const u64 u = blockIdx.x;
-    const u64 tb = u * TILE;
-    const u64 cbase = tb + (u64)wid * CH;
-
-    // (a) own tile: classify, counts, then canonical keys into sorted lists
-    double v[VV];
-    load8(w, n, cbase + (u64)lane * VV, v);
-    u32 lm = 0, hm = 0;
+    WarpSmem<T> &S = reinterpret_cast<WarpSmem<T> *>(pack_smem)[wid];
+    const u64 G = (n + CH - 1) / CH;  // chunks
+    const u64 nt = W.nt;
+    const u64 nruns = (G + RUN - 1) / RUN;
+    const dd Dtot = W.DLb[nt];
+    for (;;) {
+        u32 run = 0;
+        if (lane == 0) run = atomicAdd(queue, 1u);
+        run = __shfl_sync(0xffffffffu, run, 0);
+        if (run >= nruns) break;
+        const u64 g0 = (u64)run * RUN, g1 = g0 + RUN < G ? g0 + RUN : G;
+        // windows start empty; cursors seek on first use
+        u32 hh = 0, hc = 0, lh = 0, lc = 0;
+        u64 gh = g0 / NW < nt ? (u64)W.T1[g0 / NW] * NW : G;  // first candidate heavy chunk
+        u64 gl = (u64)W.S1[g0 / NW] * NW;                      // first candidate light chunk
+        if (gh > G) gh = G;
+        if (gl > G) gl = G;
+        double vn[VV];
+        load8(w, n, g0 * CH + (u64)lane * VV, vn);
+        for (u64 g = g0; g < g1; ++g) {
+            const u64 t = g / NW;
+            const int c = (int)(g % NW);
+            const u64 cb = g * CH;
+            double v[VV];
 #pragma unroll
-    for (int k = 0; k < VV; ++k) {
-        lm |= (u32)(v[k] >= 0.0 && v[k] <= avg) << k;
-        hm |= (u32)(v[k] > avg) << k;
-    }
-    u32 il = __popc(lm), ih = __popc(hm);
-    const u32 cl = il, chh = ih;
+            for (int k = 0; k < VV; ++k) v[k] = vn[k];
+            if (g + 1 < g1) load8(w, n, (g + 1) * CH + (u64)lane * VV, vn);
+            // ---- own chunk: global keys of both classes, compacted
+            u32 lm, hm, nl, nh;
+            {
+                const double bD0 = c ? W.mD[g - 1] : 0.0, bD1 = W.mD[g];
+                const double bE0 = c ? W.mE[g - 1] : 0.0, bE1 = W.mE[g];
+                const dd DLu = W.DLb[t], DHu = W.DHb[t];
+                double kD[VV], kE[VV], exD, exE, tD, tE;
+                lane_class<true>(v, avg, kD, lm, exD, tD, lane);
+                class_keys(kD, exD, bD0, bD1, lane);
+                lane_class<false>(v, avg, kE, hm, exE, tE, lane);
+                class_keys(kE, exE, bE0, bE1, lane);
+                const u32 cl = __popc(lm), chh = __popc(hm);
+                u32 il = cl, ih = chh;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        u32 a = __shfl_up_sync(0xffffffffu, il, d), b = __shfl_up_sync(0xffffffffu, ih, d);
-        if (lane >= d) { il += a; ih += b; }
-    }
-    if (lane == 31) {
-        P.cntL[wid] = il;
-        P.cntH[wid] = ih;
-    }
-    __syncthreads();
-    u32 offL = 0, offH = 0, nL = 0, nH = 0;
+                for (int d = 1; d < 32; d <<= 1) {
+                    u32 a = __shfl_up_sync(0xffffffffu, il, d), b = __shfl_up_sync(0xffffffffu, ih, d);
+                    if (lane >= d) { il += a; ih += b; }
+                }
+                nl = __shfl_sync(0xffffffffu, il, 31);
+                nh = __shfl_sync(0xffffffffu, ih, 31);
+                u32 rl = il - cl, rh = nl + ih - chh;
 #pragma unroll
-    for (int k = 0; k < NW; ++k) {
-        offL += k < wid ? P.cntL[k] : 0;
-        offH += k < wid ? P.cntH[k] : 0;
-        nL += P.cntL[k];
-        nH += P.cntH[k];
-    }
-    {
-        const double bD0 = wid ? W.mD[u * NW + wid - 1] : 0.0, bD1 = W.mD[u * NW + wid];
-        const double bE0 = wid ? W.mE[u * NW + wid - 1] : 0.0, bE1 = W.mE[u * NW + wid];
-        double kD[VV], kE[VV], exD, exE, tD, tE;
-        u32 m1, m2;
-        lane_class<true>(v, avg, kD, m1, exD, tD, lane);
-        class_keys(kD, exD, bD0, bD1, lane);
-        lane_class<false>(v, avg, kE, m2, exE, tE, lane);
-        class_keys(kE, exE, bE0, bE1, lane);
-        u32 rl = offL + il - cl, rh = nL + offH + ih - chh;
-#pragma unroll
-        for (int k = 0; k < VV; ++k) {
-            const u32 pos = wid * CH + lane * VV + k;
-            if ((lm >> k) & 1) {
-                P.OK[rl] = kD[k];
-                P.OP[rl] = (unsigned short)pos;
-                P.RW[pos].tw = (decltype(RowT::tw))v[k];
-                ++rl;
-            } else if ((hm >> k) & 1) {
-                P.OK[rh] = kE[k];
-                P.OP[rh] = (unsigned short)pos;
-                ++rh;
+                for (int k = 0; k < VV; ++k) {
+                    const u32 pos = lane * VV + k;
+                    if ((lm >> k) & 1) {
+                        S.OK[rl] = add_dd_d(DLu, kD[k]);
+                        S.OP[rl] = (unsigned char)pos;
+                        S.RW[pos].tw = (decltype(RowT::tw))v[k];
+                        ++rl;
+                    } else if ((hm >> k) & 1) {
+                        S.OK[rh] = add_dd_d(DHu, kE[k]);
+                        S.OP[rh] = (unsigned char)pos;
+                        ++rh;
+                    }
+                }
             }
-        }
-    }
-    __syncthreads();
-    // heavy aliases: the next heavy of the tile, else the first heavy after it
-    {
-        const u64 after = W.nextH[u];
-        for (u32 r = threadIdx.x; r < nH; r += TB) {
-            const u32 pos = P.OP[nL + r];
-            u64 a;
-            if (r + 1 < nH) a = tb + P.OP[nL + r + 1] + 1;
-            else a = (after == NONE64) ? tb + pos + 1 : after + 1;
-            P.RW[pos].alias = (AliasT)a;
-        }
-    }
-    // (b, c) resolve lights, then heavies
-    if (nL) resolve_class<T, true>(w, n, avg, W, P, u, tb, 0, nL);
-    if (nH) resolve_class<T, false>(w, n, avg, W, P, u, tb, nL, nH);
-    __syncthreads();
-    // (d) store the tile's rows: each lane its 8 consecutive rows
-    const u64 i0 = cbase + (u64)lane * VV;
-    const u32 p0 = wid * CH + lane * VV;
-    if (i0 + VV <= n) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(&P.RW[p0]);
-        uint4 *dst = reinterpret_cast<uint4 *>(rows_out + i0);
+            __syncwarp();
+            // heavy aliases: next heavy in the chunk, else after it
+            if (nh) {
+                const unsigned char fh = lane < NW ? W.mfh[t * NW + lane] : NOFH;
+                unsigned m = __ballot_sync(0xffffffffu, lane < NW && lane > c && fh != NOFH);
+                u64 after;
+                if (m) {
+                    const int cc = __ffs(m) - 1;
+                    after = t * TILE + (u64)cc * CH + (unsigned char)__shfl_sync(0xffffffffu, (int)fh, cc);
+                } else {
+                    after = W.nextH[t];
+                }
+                for (u32 r = lane; r < nh; r += 32) {
+                    const u32 pos = S.OP[nl + r];
+                    u64 a;
+                    if (r + 1 < nh) a = cb + S.OP[nl + r + 1] + 1;
+                    else a = (after == NONE64) ? cb + pos + 1 : after + 1;
+                    S.RW[pos].alias = (AliasT)a;
+                }
+            }
+            // ---- lights: alias = first heavy key > light key
+            for (u32 r0 = 0; r0 < nl;) {
+                const dd x0 = S.OK[r0], xm = S.OK[nl - 1];
+                // drop heavies with key <= x0
+                const u32 d = ring_search(S.HK, hh, hc, [&](dd k) { return dd_le(k, x0); });
+                hh = (hh + d) & (WCAP - 1);
+                hc -= d;
+                // fill until a heavy key > xm is present
+                while ((hc == 0 || dd_le(S.HK[(hh + hc - 1) & (WCAP - 1)], xm)) && gh < G &&
+                       hc + CH <= WCAP) {
+                    if (hc == 0) gh = seek_chunk<false>(W, gh, G, x0);
+                    if (gh >= G) break;
+                    hc += append_chunk<T, false>(w, n, avg, W, gh, S.HK, S.HI, hh + hc, lane);
+                    ++gh;
+                }
+                u32 r1;
+                if (hc == 0) {
+                    r1 = nl;  // no heavy key past these lights: own rows
+                    for (u32 r = r0 + lane; r < r1; r += 32) {
+                        const u32 pos = S.OP[r];
+                        S.RW[pos].alias = (AliasT)(cb + pos + 1);
+                    }
+                } else {
+                    const dd last = S.HK[(hh + hc - 1) & (WCAP - 1)];
+                    r1 = nl;
+                    if (!dd_lt(xm, last)) {  // window ends inside this chunk's lights
+                        u32 a = r0, b = nl;
+                        while (a < b) {
+                            const u32 mid = (a + b) >> 1;
+                            if (dd_lt(S.OK[mid], last)) a = mid + 1;
+                            else b = mid;
+                        }
+                        r1 = a;
+                        if (gh >= G) r1 = nl;  // nothing left to append: the rest have no heavy past them
+                    }
+                    for (u32 r = r0 + lane; r < r1; r += 32) {
+                        const dd x = S.OK[r];
+                        const u32 i = ring_search(S.HK, hh, hc, [&](dd k) { return dd_le(k, x); });
+                        const u32 pos = S.OP[r];
+                        const u64 al = i < hc ? (u64)S.HI[(hh + i) & (WCAP - 1)] + 1 : cb + pos + 1;
+                        S.RW[pos].alias = (AliasT)al;
+                    }
+                }
+                __syncwarp();
+                r0 = r1;
+            }
+            // ---- heavies: tw = key - (first light key >= heavy key) + avg
+            for (u32 r0 = 0; r0 < nh;) {
+                const dd y0 = S.OK[nl + r0], ym = S.OK[nl + nh - 1];
+                const u32 d = ring_search(S.LK, lh, lc, [&](dd k) { return dd_lt(k, y0); });
+                lh = (lh + d) & (WCAP - 1);
+                lc -= d;
+                while ((lc == 0 || dd_lt(S.LK[(lh + lc - 1) & (WCAP - 1)], ym)) && gl < G &&
+                       lc + CH <= WCAP) {
+                    if (lc == 0) gl = seek_chunk<true>(W, gl, G, y0);
+                    if (gl >= G) break;
+                    lc += append_chunk<T, true>(w, n, avg, W, gl, S.LK, nullptr, lh + lc, lane);
+                    ++gl;
+                }
+                u32 r1 = nh;
+                if (lc > 0) {
+                    const dd last = S.LK[(lh + lc - 1) & (WCAP - 1)];
+                    if (dd_lt(last, ym) && gl < G) {  // window ends inside: resolve y <= last
+                        u32 a = r0, b = nh;
+                        while (a < b) {
+                            const u32 mid = (a + b) >> 1;
+                            if (dd_le(S.OK[nl + mid], last)) a = mid + 1;
+                            else b = mid;
+                        }
+                        r1 = a;
+                    }
+                }
+                for (u32 r = r0 + lane; r < r1; r += 32) {
+                    const dd y = S.OK[nl + r];
+                    const u32 i = ring_search(S.LK, lh, lc, [&](dd k) { return dd_lt(k, y); });
+                    const dd DL = i < lc ? S.LK[(lh + i) & (WCAP - 1)] : Dtot;
+                    const dd tw = dd_add_d(dd_sub(y, DL), avg);
+                    S.RW[S.OP[nl + r]].tw = tw_store<T>(tw.hi + tw.lo, avg);
+                }
+                __syncwarp();
+                r0 = r1;
+            }
+            __syncwarp();
+            // ---- store the chunk's rows (each lane its 8 consecutive rows)
+            const u64 i0 = cb + (u64)lane * VV;
+            if (i0 + VV <= n) {
+                const uint4 *src = reinterpret_cast<const uint4 *>(&S.RW[lane * VV]);
+                uint4 *dst = reinterpret_cast<uint4 *>(rows_out + i0);
 #pragma unroll
-        for (int q = 0; q < (int)(VV * sizeof(RowT) / 16); ++q) dst[q] = src[q];
-    } else {
-        for (int k = 0; k < VV; ++k)
-            if (i0 + k < n) rows_out[i0 + k] = P.RW[p0 + k];
+                for (int q = 0; q < (int)(VV * sizeof(RowT) / 16); ++q) dst[q] = src[q];
+            } else {
+                for (int k = 0; k < VV; ++k)
+                    if (i0 + k < n) rows_out[i0 + k] = S.RW[lane * VV + k];
+            }
+            __syncwarp();
+        }
     }
 }
 
@@ -853,10 +800,17 @@ int run_build(const void *wv, u64 n, double total, void *rows, void *ws, cudaStr
     AK_LAUNCH_CHECK("k_build_scan");
     k_build_coarse<<<(unsigned)((W.nt + 1 + 255) / 256), 256, 0, st>>>(W, n);
     AK_LAUNCH_CHECK("k_build_coarse");
-    const size_t smem = sizeof(PackSmem<T>);
+    const size_t smem = sizeof(WarpSmem<T>) * PW;
     AK_CUDA_TRY(cudaFuncSetAttribute(k_build_pack<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-    k_build_pack<T><<<(unsigned)W.nt, TB, smem, st>>>(w, n, avg, W, (typename RowOf<T>::type *)rows);
+    int per_sm = 0;
+    AK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_build_pack<T>, PW * 32, smem));
+    if (per_sm < 1) per_sm = 1;
+    const u64 G = (n + CH - 1) / CH, nruns = (G + RUN - 1) / RUN;
+    u64 grid = (u64)ak_num_sms() * per_sm;
+    if (grid * PW > nruns) grid = (nruns + PW - 1) / PW;
+    k_build_pack<T><<<(unsigned)grid, PW * 32, smem, st>>>(w, n, avg, W, (typename RowOf<T>::type *)rows,
+                                                          W.counter + 1);
     AK_LAUNCH_CHECK("k_build_pack");
     return AK_OK;
 }
@@ -882,7 +836,10 @@ int ak_build_psa(const void *w, int dtype, uint64_t n, double total, void *rows,
         if (n >= 0xFFFFFFFFull) return AK_ERR_VALUE;  // u32 aliases
         return run_build<float>(w, n, total, rows, ws, st);
     }
-    if (dtype == AK_F64) return run_build<double>(w, n, total, rows, ws, st);
+    if (dtype == AK_F64) {
+        if (n >= 0xFFFFFFFFull) return AK_ERR_VALUE;  // u32 item ids in the pack windows
+        return run_build<double>(w, n, total, rows, ws, st);
+    }
     return AK_ERR_VALUE;
 }
 
