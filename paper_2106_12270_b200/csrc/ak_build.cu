@@ -34,12 +34,12 @@
 //                    the first heavy tile covering its light keys (T1) and
 //                    the first light tile covering its heavy keys (S1), and
 //                    the first heavy after it (nextH).
-//  3. k_build_pack   persistent warps stream through runs of chunks taken in
-//                    order from a global queue, resolving each own chunk
-//                    against two sliding windows of foreign keys (the heavies
-//                    after its lights, the lights at or after its heavies),
-//                    advanced chunk by chunk; rows staged in shared memory
-//                    and stored once, coalesced.
+//  3. k_build_pack   CTA per tile: rebuild the tile's keys (lights and heavies
+//                    key-sorted in shared memory); per class, rebuild the run
+//                    of foreign chunks its keys need (L2-resident: the
+//                    neighbouring CTAs own them) in the tile's own frame and
+//                    merge-path them against the own keys; rows staged in
+//                    shared memory and stored once, coalesced.
 //  DRAM traffic ~ read w twice + write the rows once = the algorithmic bytes.
 #include "ak_common.cuh"
 
@@ -70,6 +70,7 @@ struct BuildWs {
     u64 *firstH;            // [nt]
     double *mD, *mE;        // [nt*8] chunk bounds (monotone inclusive scans)
     unsigned char *mfh;     // [nt*8] first heavy offset in chunk, NOFH if none
+    unsigned short *mcl;    // [nt*8] lights in chunk
     u32 *T1, *S1;           // [nt+1]
     u64 *nextH;             // [nt]
 };
@@ -83,8 +84,8 @@ template <typename F> inline void layout(u64 n, F &&take)
     size_t sizes[19] = {256,          nst * 4,      nst * 16,       nst * 16,       nst * 8,
                         nst * 16,     nst * 16,     nst * 8,        (nt + 1) * 16,  (nt + 1) * 16,
                         (nt + 1) * 8, nt * 8,       nt * NW * 8,    nt * NW * 8,    nt * NW,
-                        (nt + 1) * 4, (nt + 1) * 4, nt * 8,         0};
-    for (int i = 0; i < 18; ++i) take(i, sizes[i]);
+                        (nt + 1) * 4, (nt + 1) * 4, nt * 8,         nt * NW * 2};
+    for (int i = 0; i < 19; ++i) take(i, sizes[i]);
 }
 
 inline BuildWs carve(void *ws, u64 n)
@@ -94,7 +95,7 @@ inline BuildWs carve(void *ws, u64 n)
     W.nst = (W.nt + SUPER - 1) / SUPER;
     char *base = (char *)ws;
     size_t off = 0;
-    char *p[18];
+    char *p[19];
     layout(n, [&](int i, size_t b) {
         p[i] = base + off;
         off += align256(b);
@@ -117,6 +118,7 @@ inline BuildWs carve(void *ws, u64 n)
     W.T1 = (u32 *)p[15];
     W.S1 = (u32 *)p[16];
     W.nextH = (u64 *)p[17];
+    W.mcl = (unsigned short *)p[18];
     return W;
 }
 
@@ -248,9 +250,6 @@ template <typename T>
 __global__ void __launch_bounds__(TB) k_build_scan(const T *__restrict__ w, u64 n, double avg,
                                                    BuildWs W)
 {
-    __shared__ double s_cD[NW], s_cE[NW];
-    __shared__ u32 s_cL[NW];
-    __shared__ unsigned char s_fh[NW];
     __shared__ double s_tD[SUPER], s_tE[SUPER];
     __shared__ u32 s_tL[SUPER];
     __shared__ u64 s_fH[SUPER];
@@ -264,64 +263,66 @@ __global__ void __launch_bounds__(TB) k_build_scan(const T *__restrict__ w, u64 
     const u64 t0 = st * SUPER;
     const u64 tn = (t0 + SUPER <= W.nt) ? SUPER : W.nt - t0;
 
-    double vnext[VV];
-    load8(w, n, t0 * TILE + (u64)threadIdx.x * VV, vnext);
-    for (u64 j = 0; j < tn; ++j) {
+    // each warp owns whole tiles (no per-tile block barrier): 8 chunk totals
+    // by butterfly sums, then their monotone scan within the warp
+    for (u64 j = wid; j < tn; j += NW) {
         const u64 t = t0 + j;
-        double v[VV];
+        double cd = 0.0, ce = 0.0;  // lane c < 8 ends up holding chunk c's totals
+        u32 cl = 0;
+        unsigned char cf = NOFH;
+        double va[VV], vb[VV];
+        load8(w, n, t * TILE + (u64)lane * VV, va);
 #pragma unroll
-        for (int k = 0; k < VV; ++k) v[k] = vnext[k];
-        if (j + 1 < tn) load8(w, n, (t + 1) * TILE + (u64)threadIdx.x * VV, vnext);
-        u32 lm, hm;
-        const double totD = chunk_total<true>(v, avg, lm);
-        const double totE = chunk_total<false>(v, avg, hm);
-        u32 nl = __popc(lm);
+        for (int c = 0; c < NW; ++c) {
+            double *v = (c & 1) ? vb : va;
+            if (c + 1 < NW) load8(w, n, t * TILE + (u64)(c + 1) * CH + (u64)lane * VV, (c & 1) ? va : vb);
+            u32 lm, hm;
+            const double tD = chunk_total<true>(v, avg, lm);
+            const double tE = chunk_total<false>(v, avg, hm);
+            u32 nl = __popc(lm);
 #pragma unroll
-        for (int d = 16; d >= 1; d >>= 1) nl += __shfl_xor_sync(0xffffffffu, nl, d);
-        const unsigned char fh = first_item(hm, lane);
+            for (int d = 16; d >= 1; d >>= 1) nl += __shfl_xor_sync(0xffffffffu, nl, d);
+            const unsigned char fh = first_item(hm, lane);
+            if (lane == c) {
+                cd = tD;
+                ce = tE;
+                cl = nl;
+                cf = fh;
+            }
+        }
+        // monotone scan of the 8 chunk totals -> chunk bounds
+        double x = lane < NW ? cd : 0.0, y = lane < NW ? ce : 0.0;
+#pragma unroll
+        for (int d = 1; d < NW; d <<= 1) {
+            double a = shfl_up_d(x, d), b = shfl_up_d(y, d);
+            if (lane >= d) { x = x + a; y = y + b; }
+        }
+#pragma unroll
+        for (int d = 1; d < NW; d <<= 1) {
+            double a = shfl_up_d(x, d), b = shfl_up_d(y, d);
+            if (lane >= d) { x = fmax(x, a); y = fmax(y, b); }
+        }
+        if (lane < NW) {
+            W.mD[t * NW + lane] = x;
+            W.mE[t * NW + lane] = y;
+            W.mfh[t * NW + lane] = cf;
+            W.mcl[t * NW + lane] = (unsigned short)cl;
+        }
+        u32 tl = lane < NW ? cl : 0;
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) tl += __shfl_xor_sync(0xffffffffu, tl, d);
+        const unsigned fhm = __ballot_sync(0xffffffffu, lane < NW && cf != NOFH);
+        const int fc = fhm ? __ffs(fhm) - 1 : 0;
+        const unsigned char ff = (unsigned char)__shfl_sync(0xffffffffu, (int)cf, fc);
+        const double tD = shfl_idx_d(x, NW - 1), tE = shfl_idx_d(y, NW - 1);
         if (lane == 0) {
-            s_cD[wid] = totD;
-            s_cE[wid] = totE;
-            s_cL[wid] = nl;
-            s_fh[wid] = fh;
+            s_tD[j] = tD;
+            s_tE[j] = tE;
+            s_tL[j] = tl;
+            s_fH[j] = fhm ? t * TILE + (u64)fc * CH + ff : NONE64;
         }
-        __syncthreads();
-        if (wid == 0) {
-            // monotone scan of the chunk totals -> chunk bounds
-            double x = lane < NW ? s_cD[lane] : 0.0, y = lane < NW ? s_cE[lane] : 0.0;
-#pragma unroll
-            for (int d = 1; d < NW; d <<= 1) {
-                double a = shfl_up_d(x, d), b = shfl_up_d(y, d);
-                if (lane >= d) { x = x + a; y = y + b; }
-            }
-#pragma unroll
-            for (int d = 1; d < NW; d <<= 1) {
-                double a = shfl_up_d(x, d), b = shfl_up_d(y, d);
-                if (lane >= d) { x = fmax(x, a); y = fmax(y, b); }
-            }
-            const unsigned char f = lane < NW ? s_fh[lane] : NOFH;
-            if (lane < NW) {
-                W.mD[t * NW + lane] = x;
-                W.mE[t * NW + lane] = y;
-                W.mfh[t * NW + lane] = f;
-            }
-            u32 cl = lane < NW ? s_cL[lane] : 0;
-#pragma unroll
-            for (int d = 16; d >= 1; d >>= 1) cl += __shfl_xor_sync(0xffffffffu, cl, d);
-            unsigned fhm = __ballot_sync(0xffffffffu, lane < NW && f != NOFH);
-            const int c = fhm ? __ffs(fhm) - 1 : 0;
-            const unsigned char fc = (unsigned char)__shfl_sync(0xffffffffu, (int)f, c);
-            if (lane == NW - 1) {
-                s_tD[j] = x;
-                s_tE[j] = y;
-            }
-            if (lane == 0) {
-                s_tL[j] = cl;
-                s_fH[j] = fhm ? t * TILE + (u64)c * CH + fc : NONE64;
-            }
-        }
-        __syncthreads();
     }
+    __syncthreads();
     // super-tile aggregate: exact double-double sum of the tile totals
     if (threadIdx.x == 0) {
         dd aD = dd_make(0.0), aH = dd_make(0.0);
@@ -472,30 +473,48 @@ __global__ void k_build_coarse(BuildWs W, u64 n)
 }
 
 // ---------------------------------------------------------------------------
-// 3. warp-streaming pack
+// 3. tile pack: merge-path against the needed foreign chunks
 // ---------------------------------------------------------------------------
-// Every warp takes runs of RUN consecutive chunks from a global queue (runs
-// are handed out in order, so the runs in flight — and the foreign chunks
-// they read — stay L2-resident) and streams through them.  It keeps two
-// warp-private sliding windows of global double-double keys:
-//   HW: the heavies following its current lights in key order,
-//   LW: the lights at or after its current heavies in key order,
-// each advanced monotonically by rebuilding the canonical keys of the next
-// foreign chunk of that class (chunks whose key range lies entirely behind
-// the request are skipped via the pass-1 chunk bounds).  An own chunk is
-// resolved against the windows and its 256 rows are stored once, coalesced.
-// No block barriers: warps are independent.
-constexpr int RUN = 16;          // chunks per queue item
-constexpr int WCAP = 512;        // window capacity (entries); a chunk adds <= 256
-constexpr int PW = 4;            // warps per CTA
+// One CTA owns one tile (8 warps).  (a) The warps rebuild the tile's
+// canonical keys; lights and heavies are laid out key-sorted in shared
+// memory.  (b) Per class, the own keys [x_min, x_max] need a contiguous run
+// of foreign chunks of the other class (the chunk holding the first key past
+// x_min through the one holding the first key past x_max).  Dense path: the
+// warps rebuild those chunks' keys once, converted into the tile's own frame
+// (exact double-doubles), at offsets known from the pass-1 chunk counts; one
+// CTA-wide merge path then gives every own element its successor.  Sparse
+// path (the run is too long, e.g. next to a giant heavy): every own element
+// gets its target chunk, equal targets form groups, and a warp resolves each
+// group against its one chunk.  (c) The rows are stored once, coalesced.
+constexpr int MAXSLOT = 4;       // candidate foreign tiles with cached bounds
+constexpr int GCAP = 256;        // groups per round (sparse path)
+constexpr int FCAP = 1280;       // foreign keys per merge (dense path)
+constexpr int MAXRUN = 32;       // foreign chunks per merge (dense path)
+constexpr u32 TG_NONE = 0xFFFFFFFFu;
 
-template <typename T> struct WarpSmem {
-    dd OK[CH];                        // own global keys: lights [0,nl), heavies [nl,nl+nh)
-    dd HK[WCAP];                      // heavy window keys (ring)
-    dd LK[WCAP];                      // light window keys (ring)
-    typename RowOf<T>::type RW[CH];   // staged rows
-    u32 HI[WCAP];                     // heavy window items (0-based)
-    unsigned char OP[CH];             // own item offsets
+template <typename T> struct PackSmem {
+    double OK[TILE];                    // own keys (tile-local): lights [0,nL), heavies [nL,nL+nH)
+    typename RowOf<T>::type RW[TILE];   // staged rows
+    unsigned short OP[TILE];            // own item offsets
+    union {
+        struct {                        // dense path
+            dd FK[FCAP];                // foreign keys in the own frame
+            u32 FI[FCAP];               // foreign heavy items (0-based, low 32 bits)
+            u32 off[MAXRUN + 1];        // per-chunk offsets into FK
+        } d;
+        struct {                        // sparse path
+            double F[NW][CH];
+            u32 TG[TILE];
+            unsigned char FP[NW][CH];
+            u32 GT[GCAP];
+            unsigned short GS[GCAP + 1];
+        } s;
+    } u;
+    dd SB[MAXSLOT * NW];                // own-frame chunk bounds of the candidate tiles
+    dd sent;                            // dense sentinel key (lights: bound after the run)
+    u64 sent_item;                      // dense sentinel item (heavies: next heavy after the run)
+    u32 cnt[NW], cnt2[NW];
+    u32 gA, gB, dense, nf;
 };
 
 // d + x as a normalised double-double (exact for the key ranges in play)
@@ -508,283 +527,446 @@ __device__ __forceinline__ dd add_dd_d(dd d, double x)
     fast_two_sum(s, e, h, l);
     return dd_make(h, l);
 }
+// f <= X and f < X for normalised X (double vs double-double)
+__device__ __forceinline__ bool le_d_dd(double f, dd X) { return f < X.hi || (f == X.hi && X.lo >= 0.0); }
+__device__ __forceinline__ bool lt_d_dd(double f, dd X) { return f < X.hi || (f == X.hi && X.lo > 0.0); }
+// X <= f and X < f
+__device__ __forceinline__ bool le_dd_d(dd X, double f) { return X.hi < f || (X.hi == f && X.lo <= 0.0); }
+__device__ __forceinline__ bool lt_dd_d(dd X, double f) { return X.hi < f || (X.hi == f && X.lo < 0.0); }
 
-__device__ __forceinline__ dd chunk_base(const BuildWs &W, u64 g, bool light, bool upper)
+// first heavy item (0-based) after chunk c of tile t (NONE64 if none)
+__device__ __forceinline__ u64 next_heavy_after(const BuildWs &W, u64 t, int c, int lane)
 {
-    // global lower (upper) bound of the keys of one class in chunk g
-    const u64 t = g / NW;
-    const int c = (int)(g % NW);
-    const double *mB = light ? W.mD : W.mE;
-    const double loc = upper ? mB[g] : (c ? mB[g - 1] : 0.0);
-    return add_dd_d(light ? W.DLb[t] : W.DHb[t], loc);
+    const unsigned char fh = lane < NW ? W.mfh[t * NW + lane] : NOFH;
+    unsigned m = __ballot_sync(0xffffffffu, lane < NW && lane > c && fh != NOFH);
+    if (m) {
+        int cc = __ffs(m) - 1;
+        unsigned char f = (unsigned char)__shfl_sync(0xffffffffu, (int)fh, cc);
+        return t * TILE + (u64)cc * CH + f;
+    }
+    return W.nextH[t];
 }
 
-// Canonical global keys of one class of chunk g, appended to a window ring.
-// Returns the number appended.
+// Canonical (tile-local) keys of one class of chunk (t, c) and their mask.
 template <typename T, bool LIGHT>
-__device__ __forceinline__ u32 append_chunk(const T *__restrict__ w, u64 n, double avg,
-                                            const BuildWs &W, u64 g, dd *K, u32 *I, u32 tail,
-                                            int lane)
+__device__ __forceinline__ u32 chunk_keys(const T *__restrict__ w, u64 n, double avg,
+                                          const BuildWs &W, u64 t, int c, double k[VV], int lane)
 {
-    const u64 t = g / NW;
-    const int c = (int)(g % NW);
     const double *mB = LIGHT ? W.mD : W.mE;
-    const double base = c ? mB[g - 1] : 0.0, bound = mB[g];
-    const dd B = LIGHT ? W.DLb[t] : W.DHb[t];
-    double v[VV], k[VV], ex, tot;
+    const double base = c ? mB[t * NW + c - 1] : 0.0, bound = mB[t * NW + c];
+    double v[VV], ex, tot;
     u32 m;
-    load8(w, n, g * CH + (u64)lane * VV, v);
+    load8(w, n, t * TILE + (u64)c * CH + (u64)lane * VV, v);
     lane_class<LIGHT>(v, avg, k, m, ex, tot, lane);
     class_keys(k, ex, base, bound, lane);
-    const u32 cnt = __popc(m);
+    return m;
+}
+
+__device__ __forceinline__ u32 warp_excl_count(u32 cnt, u32 &total, int lane)
+{
     u32 inc = cnt;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
         u32 a = __shfl_up_sync(0xffffffffu, inc, d);
         if (lane >= d) inc += a;
     }
-    const u32 total = __shfl_sync(0xffffffffu, inc, 31);
-    u32 r = tail + inc - cnt;
-#pragma unroll
-    for (int q = 0; q < VV; ++q)
-        if ((m >> q) & 1) {
-            const u32 s = r & (WCAP - 1);
-            K[s] = add_dd_d(B, k[q]);
-            if (!LIGHT) I[s] = (u32)(g * CH + lane * VV + q);
-            ++r;
-        }
-    __syncwarp();
-    return total;
+    total = __shfl_sync(0xffffffffu, inc, 31);
+    return inc - cnt;
 }
 
-// first index i in [0, cnt) of the ring (from head) with pred(K[i]) false,
-// pred monotone (true then false); warp-uniform
-template <typename P>
-__device__ __forceinline__ u32 ring_search(const dd *K, u32 head, u32 cnt, P pred)
+// Target chunk of own key x (tile-local, own frame): the foreign chunk of
+// the other class holding the first key past x (ISL: first heavy key > x;
+// else first light key >= x), TG_NONE if beyond every chunk.
+template <bool ISL>
+__device__ u32 target_of(const BuildWs &W, const dd *SB, bool fast, u32 nslot, u64 fT0, u64 fT1,
+                         dd DLu, dd DHu, double x)
 {
-    u32 a = 0, b = cnt;
+    const u64 nt = W.nt;
+    if (fast) {
+        u32 a = 0, b = nslot * NW;
+        while (a < b) {
+            const u32 mid = (a + b) >> 1;
+            const bool before = ISL ? !lt_d_dd(x, SB[mid]) : !le_d_dd(x, SB[mid]);
+            if (before) a = mid + 1;
+            else b = mid;
+        }
+        if (a < nslot * NW) {
+            const u64 t = fT0 + a / NW;
+            return t < nt ? (u32)(t * NW + a % NW) : TG_NONE;
+        }
+        return TG_NONE;
+    }
+    u64 a = fT0, b = fT1 + 1;
     while (a < b) {
-        const u32 mid = (a + b) >> 1;
-        if (pred(K[(head + mid) & (WCAP - 1)])) a = mid + 1;
+        const u64 mid = (a + b) >> 1;
+        bool before;
+        if (mid >= nt) before = false;
+        else {
+            const dd L = ISL ? dd_sub(W.DHb[mid + 1], DLu) : dd_sub(W.DLb[mid + 1], DHu);
+            before = ISL ? !lt_d_dd(x, L) : !le_d_dd(x, L);
+        }
+        if (before) a = mid + 1;
         else b = mid;
     }
-    return a;
+    if (a > fT1 || a >= nt) return TG_NONE;
+    const dd D = ISL ? dd_sub(W.DHb[a], DLu) : dd_sub(W.DLb[a], DHu);  // foreign base - own base
+    const double *mB = (ISL ? W.mE : W.mD) + a * NW;
+    int c = 0;
+    for (; c < NW - 1; ++c) {
+        const dd B = add_dd_d(D, mB[c]);
+        if (ISL ? lt_d_dd(x, B) : le_d_dd(x, B)) break;
+    }
+    return (u32)(a * NW + c);
 }
 
-// seek: first chunk g >= from whose class bound passes key x
-// (heavies: bound > x; lights: bound >= x), G if none
-template <bool LIGHT>
-__device__ u64 seek_chunk(const BuildWs &W, u64 from, u64 G, dd x)
+template <typename T, bool ISL>
+__device__ void resolve_class(const T *__restrict__ w, u64 n, double avg, const BuildWs &W,
+                              PackSmem<T> &P, u64 u, u64 tb, u32 ob, u32 cnt)
 {
-    auto passes = [&](u64 g) {
-        const dd b = chunk_base(W, g, LIGHT, true);
-        return LIGHT ? !dd_lt(b, x) : dd_lt(x, b);
-    };
-    if (from >= G || passes(from)) return from;
-    // gallop, then bisect
-    u64 lo = from, step = 1;  // invariant: !passes(lo)
-    while (lo + step < G && !passes(lo + step)) {
-        lo += step;
-        step <<= 1;
+    typedef typename RowOf<T>::type RowT;
+    typedef decltype(RowT::alias) AliasT;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const u64 nt = W.nt;
+    const dd DLu = W.DLb[u], DHu = W.DHb[u];
+    const dd own_base = ISL ? DLu : DHu;
+    const u64 fT0 = ISL ? W.T1[u] : W.S1[u];
+    const u64 fT1 = ISL ? W.T1[u + 1] : W.S1[u + 1];
+    // foreign base - own base: a foreign local key f is f + Dn in the own frame
+    auto Dn = [&](u64 t) -> dd { return dd_sub(ISL ? W.DHb[t] : W.DLb[t], own_base); };
+    const bool fast = fT1 - fT0 + 1 <= (u64)MAXSLOT;
+    const u32 nslot = fast ? (u32)(fT1 - fT0 + 1) : 0;
+    if (fast) {
+        for (u32 i = threadIdx.x; i < nslot * NW; i += TB) {
+            const u64 t = fT0 + i / NW;
+            P.SB[i] = t >= nt ? dd_make(INFINITY, 0.0)
+                              : add_dd_d(Dn(t), (ISL ? W.mE : W.mD)[t * NW + i % NW]);
+        }
     }
-    u64 hi = lo + step < G ? lo + step : G;  // passes(hi) or hi == G
-    while (hi - lo > 1) {
-        const u64 mid = (lo + hi) >> 1;
-        if (passes(mid)) hi = mid;
-        else lo = mid;
+    __syncthreads();
+    // ---- the run of foreign chunks needed by [x_min, x_max]
+    if (threadIdx.x == 0) {
+        const u32 a = target_of<ISL>(W, P.SB, fast, nslot, fT0, fT1, DLu, DHu, P.OK[ob]);
+        u32 b = target_of<ISL>(W, P.SB, fast, nslot, fT0, fT1, DLu, DHu, P.OK[ob + cnt - 1]);
+        u32 dense = 0, nf = 0;
+        if (a != TG_NONE) {
+            bool tail_none = b == TG_NONE;
+            if (tail_none) b = (u32)(nt * NW - 1);
+            if (b >= a && b - a + 1 <= (u32)MAXRUN) {
+                // foreign counts of the run
+                u32 off = 0;
+                for (u32 g = a; g <= b; ++g) {
+                    P.u.d.off[g - a] = off;
+                    const u64 cs = (u64)g * CH;
+                    const u32 valid = (u32)(n - cs < (u64)CH ? n - cs : (u64)CH);
+                    const u32 nlc = W.mcl[g];
+                    off += ISL ? valid - nlc : nlc;
+                }
+                P.u.d.off[b - a + 1] = off;
+                if (off <= (u32)FCAP) {
+                    dense = 1;
+                    nf = off;
+                    const u64 tb_ = b / NW;
+                    const int cb_ = (int)(b % NW);
+                    if (ISL) {
+                        P.sent_item = tail_none ? NONE64 : W.nextH[tb_];  // refined below
+                    } else {
+                        P.sent = tail_none ? dd_sub(W.DLb[nt], DHu)
+                                           : add_dd_d(Dn(tb_), W.mD[b]);
+                    }
+                    (void)cb_;
+                }
+            }
+            if (tail_none) b = TG_NONE;
+        }
+        P.gA = a;
+        P.gB = b;
+        P.dense = dense;
+        P.nf = nf;
     }
-    return hi;
+    __syncthreads();
+    const u32 gA = P.gA, gB = P.gB;
+    if (gA == TG_NONE) {
+        // no foreign key past any own key
+        for (u32 r = threadIdx.x; r < cnt; r += TB) {
+            const u32 pos = P.OP[ob + r];
+            if (ISL) {
+                P.RW[pos].alias = (AliasT)(tb + pos + 1);
+            } else {
+                const dd tw = dd_add_d(add_dd_d(dd_neg(dd_sub(W.DLb[nt], DHu)), P.OK[ob + r]), avg);
+                P.RW[pos].tw = tw_store<T>(tw.hi + tw.lo, avg);
+            }
+        }
+        __syncthreads();
+        return;
+    }
+    if (P.dense) {
+        const u32 nf = P.nf;
+        const u32 gEnd = gB == TG_NONE ? (u32)(nt * NW - 1) : gB;
+        if (ISL && gB != TG_NONE && wid == 0) {
+            const u64 sa = next_heavy_after(W, gB / NW, (int)(gB % NW), lane);
+            if (lane == 0) P.sent_item = sa;
+        }
+        // rebuild the run's keys, into the own frame
+        for (u32 g = gA + wid; g <= gEnd; g += NW) {
+            const u64 t = g / NW;
+            const int c = (int)(g % NW);
+            double k[VV];
+            const u32 m = chunk_keys<T, !ISL>(w, n, avg, W, t, c, k, lane);
+            u32 tot;
+            u32 r = P.u.d.off[g - gA] + warp_excl_count(__popc(m), tot, lane);
+            const dd D = Dn(t);
+#pragma unroll
+            for (int q = 0; q < VV; ++q)
+                if ((m >> q) & 1) {
+                    P.u.d.FK[r] = add_dd_d(D, k[q]);
+                    if (ISL) P.u.d.FI[r] = (u32)((u64)g * CH + lane * VV + q);
+                    ++r;
+                }
+        }
+        __syncthreads();
+        // merge path: own [0,cnt) with foreign [0,nf); foreign first when
+        //   ISL: F <= x (heavy closes before the light);  else F < y
+        const u32 total = cnt + nf;
+        const u32 per = (total + TB - 1) / TB;
+        const u32 d0 = threadIdx.x * per;
+        if (d0 < total) {
+            u32 lo = d0 > nf ? d0 - nf : 0, hi = d0 < cnt ? d0 : cnt;
+            while (lo < hi) {
+                const u32 mid = (lo + hi) >> 1;
+                const u32 j = d0 - mid - 1;  // own[mid] precedes foreign[j]?
+                const dd Fj = P.u.d.FK[j];
+                const bool own_first = ISL ? !le_dd_d(Fj, P.OK[ob + mid]) : !lt_dd_d(Fj, P.OK[ob + mid]);
+                if (own_first) lo = mid + 1;
+                else hi = mid;
+            }
+            u32 i = lo, j = d0 - lo;
+            const u32 d1 = d0 + per < total ? d0 + per : total;
+            for (u32 d = d0; d < d1; ++d) {
+                bool take_own;
+                if (i >= cnt) take_own = false;
+                else if (j >= nf) take_own = true;
+                else {
+                    const dd Fj = P.u.d.FK[j];
+                    take_own = ISL ? !le_dd_d(Fj, P.OK[ob + i]) : !lt_dd_d(Fj, P.OK[ob + i]);
+                }
+                if (!take_own) {
+                    ++j;
+                    continue;
+                }
+                const u32 pos = P.OP[ob + i];
+                if (ISL) {
+                    u64 al;
+                    if (j < nf) al = (u64)P.u.d.FI[j] + 1;
+                    else al = P.sent_item == NONE64 ? tb + pos + 1 : P.sent_item + 1;
+                    P.RW[pos].alias = (AliasT)al;
+                } else {
+                    const dd DL = j < nf ? P.u.d.FK[j] : P.sent;
+                    const dd tw = dd_add_d(add_dd_d(dd_neg(DL), P.OK[ob + i]), avg);
+                    P.RW[pos].tw = tw_store<T>(tw.hi + tw.lo, avg);
+                }
+                ++i;
+            }
+        }
+        __syncthreads();
+        return;
+    }
+    // ---- sparse path: per-element targets, grouped
+    for (u32 i = threadIdx.x; i < cnt; i += TB)
+        P.u.s.TG[i] = target_of<ISL>(W, P.SB, fast, nslot, fT0, fT1, DLu, DHu, P.OK[ob + i]);
+    __syncthreads();
+    u32 e0 = 0;
+    while (e0 < cnt) {
+        const u32 per = (cnt - e0 + TB - 1) / TB;
+        const u32 i0 = e0 + threadIdx.x * per, i1 = min(i0 + per, cnt);
+        u32 nst = 0;
+        for (u32 i = i0; i < i1; ++i) nst += (i == e0 || P.u.s.TG[i] != P.u.s.TG[i - 1]);
+        u32 wt;
+        const u32 ex = warp_excl_count(nst, wt, lane);
+        if (lane == 0) P.cnt2[wid] = wt;
+        __syncthreads();
+        u32 wbase = 0, tot = 0;
+        for (int k = 0; k < NW; ++k) {
+            wbase += k < wid ? P.cnt2[k] : 0;
+            tot += P.cnt2[k];
+        }
+        u32 g = wbase + ex;
+        for (u32 i = i0; i < i1; ++i)
+            if (i == e0 || P.u.s.TG[i] != P.u.s.TG[i - 1]) {
+                if (g < GCAP) {
+                    P.u.s.GS[g] = (unsigned short)i;
+                    P.u.s.GT[g] = P.u.s.TG[i];
+                }
+                ++g;
+            }
+        __syncthreads();
+        const u32 ngr = tot <= GCAP ? tot : GCAP - 1;
+        const u32 e1 = tot <= GCAP ? cnt : P.u.s.GS[GCAP - 1];
+        __syncthreads();
+        if (threadIdx.x == 0) P.u.s.GS[ngr] = (unsigned short)e1;
+        __syncthreads();
+        for (u32 gi = wid; gi < ngr; gi += NW) {
+            const u32 ga = P.u.s.GS[gi], gb = P.u.s.GS[gi + 1];
+            const u32 tgt = P.u.s.GT[gi];
+            if (tgt == TG_NONE) {
+                for (u32 r = ga + lane; r < gb; r += 32) {
+                    const u32 pos = P.OP[ob + r];
+                    if (ISL) {
+                        P.RW[pos].alias = (AliasT)(tb + pos + 1);
+                    } else {
+                        const dd tw = dd_add_d(add_dd_d(dd_neg(dd_sub(W.DLb[nt], DHu)), P.OK[ob + r]), avg);
+                        P.RW[pos].tw = tw_store<T>(tw.hi + tw.lo, avg);
+                    }
+                }
+                continue;
+            }
+            const u64 t = tgt / NW;
+            const int c = (int)(tgt % NW);
+            double *F = P.u.s.F[wid];
+            unsigned char *FP = P.u.s.FP[wid];
+            double k[VV];
+            const u32 m = chunk_keys<T, !ISL>(w, n, avg, W, t, c, k, lane);
+            u32 nF;
+            u32 r = warp_excl_count(__popc(m), nF, lane);
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < VV; ++q)
+                if ((m >> q) & 1) {
+                    F[r] = k[q];
+                    FP[r] = (unsigned char)(lane * VV + q);
+                    ++r;
+                }
+            __syncwarp();
+            const dd Do = dd_neg(Dn(t));  // own frame -> foreign frame: x - Dn
+            if (ISL) {
+                const u64 after = next_heavy_after(W, t, c, lane);
+                const u64 fb = t * TILE + (u64)c * CH;
+                for (u32 r2 = ga + lane; r2 < gb; r2 += 32) {
+                    const dd X = add_dd_d(Do, P.OK[ob + r2]);
+                    u32 a = 0, b = nF;  // first heavy key > X
+                    while (a < b) {
+                        const u32 mid = (a + b) >> 1;
+                        if (le_d_dd(F[mid], X)) a = mid + 1;
+                        else b = mid;
+                    }
+                    const u32 pos = P.OP[ob + r2];
+                    u64 al;
+                    if (a < nF) al = fb + FP[a] + 1;
+                    else al = (after == NONE64) ? tb + pos + 1 : after + 1;
+                    P.RW[pos].alias = (AliasT)al;
+                }
+            } else {
+                const double bound = W.mD[t * NW + c];
+                for (u32 r2 = ga + lane; r2 < gb; r2 += 32) {
+                    const dd Y = add_dd_d(Do, P.OK[ob + r2]);
+                    u32 a = 0, b = nF;  // first light key >= Y
+                    while (a < b) {
+                        const u32 mid = (a + b) >> 1;
+                        if (lt_d_dd(F[mid], Y)) a = mid + 1;
+                        else b = mid;
+                    }
+                    const double DL = a < nF ? F[a] : bound;
+                    const dd tw = dd_add_d(add_dd_d(Y, -DL), avg);
+                    P.RW[P.OP[ob + r2]].tw = tw_store<T>(tw.hi + tw.lo, avg);
+                }
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        e0 = e1;
+    }
 }
 
 template <typename T>
-__global__ void __launch_bounds__(PW * 32) k_build_pack(const T *__restrict__ w, u64 n,
-                                                        double avg, BuildWs W,
-                                                        typename RowOf<T>::type *__restrict__ rows_out,
-                                                        unsigned int *queue)
+__global__ void __launch_bounds__(TB, 3) k_build_pack(const T *__restrict__ w, u64 n, double avg,
+                                                      BuildWs W,
+                                                      typename RowOf<T>::type *__restrict__ rows_out)
 {
     typedef typename RowOf<T>::type RowT;
     typedef decltype(RowT::alias) AliasT;
     extern __shared__ __align__(16) unsigned char pack_smem[];
+    PackSmem<T> &P = *reinterpret_cast<PackSmem<T> *>(pack_smem);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    WarpSmem<T> &S = reinterpret_cast<WarpSmem<T> *>(pack_smem)[wid];
-    const u64 G = (n + CH - 1) / CH;  // chunks
-    const u64 nt = W.nt;
-    const u64 nruns = (G + RUN - 1) / RUN;
-    const dd Dtot = W.DLb[nt];
-    for (;;) {
-        u32 run = 0;
-        if (lane == 0) run = atomicAdd(queue, 1u);
-        run = __shfl_sync(0xffffffffu, run, 0);
-        if (run >= nruns) break;
-        const u64 g0 = (u64)run * RUN, g1 = g0 + RUN < G ? g0 + RUN : G;
-        // windows start empty; cursors seek on first use
-        u32 hh = 0, hc = 0, lh = 0, lc = 0;
-        u64 gh = g0 / NW < nt ? (u64)W.T1[g0 / NW] * NW : G;  // first candidate heavy chunk
-        u64 gl = (u64)W.S1[g0 / NW] * NW;                      // first candidate light chunk
-        if (gh > G) gh = G;
-        if (gl > G) gl = G;
-        double vn[VV];
-        load8(w, n, g0 * CH + (u64)lane * VV, vn);
-        for (u64 g = g0; g < g1; ++g) {
-            const u64 t = g / NW;
-            const int c = (int)(g % NW);
-            const u64 cb = g * CH;
-            double v[VV];
+    const u64 u = blockIdx.x;
+    const u64 tb = u * TILE;
+    const u64 cbase = tb + (u64)wid * CH;
+
+    // (a) own tile: classify, counts, then canonical keys into sorted lists
+    double v[VV];
+    load8(w, n, cbase + (u64)lane * VV, v);
+    u32 lm = 0, hm = 0;
 #pragma unroll
-            for (int k = 0; k < VV; ++k) v[k] = vn[k];
-            if (g + 1 < g1) load8(w, n, (g + 1) * CH + (u64)lane * VV, vn);
-            // ---- own chunk: global keys of both classes, compacted
-            u32 lm, hm, nl, nh;
-            {
-                const double bD0 = c ? W.mD[g - 1] : 0.0, bD1 = W.mD[g];
-                const double bE0 = c ? W.mE[g - 1] : 0.0, bE1 = W.mE[g];
-                const dd DLu = W.DLb[t], DHu = W.DHb[t];
-                double kD[VV], kE[VV], exD, exE, tD, tE;
-                lane_class<true>(v, avg, kD, lm, exD, tD, lane);
-                class_keys(kD, exD, bD0, bD1, lane);
-                lane_class<false>(v, avg, kE, hm, exE, tE, lane);
-                class_keys(kE, exE, bE0, bE1, lane);
-                const u32 cl = __popc(lm), chh = __popc(hm);
-                u32 il = cl, ih = chh;
+    for (int k = 0; k < VV; ++k) {
+        lm |= (u32)(v[k] >= 0.0 && v[k] <= avg) << k;
+        hm |= (u32)(v[k] > avg) << k;
+    }
+    u32 wl, wh;
+    const u32 el = warp_excl_count(__popc(lm), wl, lane);
+    const u32 eh = warp_excl_count(__popc(hm), wh, lane);
+    if (lane == 0) {
+        P.cnt[wid] = wl;
+        P.cnt2[wid] = wh;
+    }
+    __syncthreads();
+    u32 offL = 0, offH = 0, nL = 0, nH = 0;
 #pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    u32 a = __shfl_up_sync(0xffffffffu, il, d), b = __shfl_up_sync(0xffffffffu, ih, d);
-                    if (lane >= d) { il += a; ih += b; }
-                }
-                nl = __shfl_sync(0xffffffffu, il, 31);
-                nh = __shfl_sync(0xffffffffu, ih, 31);
-                u32 rl = il - cl, rh = nl + ih - chh;
+    for (int k = 0; k < NW; ++k) {
+        offL += k < wid ? P.cnt[k] : 0;
+        offH += k < wid ? P.cnt2[k] : 0;
+        nL += P.cnt[k];
+        nH += P.cnt2[k];
+    }
+    {
+        const double bD0 = wid ? W.mD[u * NW + wid - 1] : 0.0, bD1 = W.mD[u * NW + wid];
+        const double bE0 = wid ? W.mE[u * NW + wid - 1] : 0.0, bE1 = W.mE[u * NW + wid];
+        double kD[VV], kE[VV], exD, exE, tD, tE;
+        u32 m1, m2;
+        lane_class<true>(v, avg, kD, m1, exD, tD, lane);
+        class_keys(kD, exD, bD0, bD1, lane);
+        lane_class<false>(v, avg, kE, m2, exE, tE, lane);
+        class_keys(kE, exE, bE0, bE1, lane);
+        u32 rl = offL + el, rh = nL + offH + eh;
 #pragma unroll
-                for (int k = 0; k < VV; ++k) {
-                    const u32 pos = lane * VV + k;
-                    if ((lm >> k) & 1) {
-                        S.OK[rl] = add_dd_d(DLu, kD[k]);
-                        S.OP[rl] = (unsigned char)pos;
-                        S.RW[pos].tw = (decltype(RowT::tw))v[k];
-                        ++rl;
-                    } else if ((hm >> k) & 1) {
-                        S.OK[rh] = add_dd_d(DHu, kE[k]);
-                        S.OP[rh] = (unsigned char)pos;
-                        ++rh;
-                    }
-                }
+        for (int k = 0; k < VV; ++k) {
+            const u32 pos = wid * CH + lane * VV + k;
+            if ((lm >> k) & 1) {
+                P.OK[rl] = kD[k];
+                P.OP[rl] = (unsigned short)pos;
+                P.RW[pos].tw = (decltype(RowT::tw))v[k];
+                ++rl;
+            } else if ((hm >> k) & 1) {
+                P.OK[rh] = kE[k];
+                P.OP[rh] = (unsigned short)pos;
+                ++rh;
             }
-            __syncwarp();
-            // heavy aliases: next heavy in the chunk, else after it
-            if (nh) {
-                const unsigned char fh = lane < NW ? W.mfh[t * NW + lane] : NOFH;
-                unsigned m = __ballot_sync(0xffffffffu, lane < NW && lane > c && fh != NOFH);
-                u64 after;
-                if (m) {
-                    const int cc = __ffs(m) - 1;
-                    after = t * TILE + (u64)cc * CH + (unsigned char)__shfl_sync(0xffffffffu, (int)fh, cc);
-                } else {
-                    after = W.nextH[t];
-                }
-                for (u32 r = lane; r < nh; r += 32) {
-                    const u32 pos = S.OP[nl + r];
-                    u64 a;
-                    if (r + 1 < nh) a = cb + S.OP[nl + r + 1] + 1;
-                    else a = (after == NONE64) ? cb + pos + 1 : after + 1;
-                    S.RW[pos].alias = (AliasT)a;
-                }
-            }
-            // ---- lights: alias = first heavy key > light key
-            for (u32 r0 = 0; r0 < nl;) {
-                const dd x0 = S.OK[r0], xm = S.OK[nl - 1];
-                // drop heavies with key <= x0
-                const u32 d = ring_search(S.HK, hh, hc, [&](dd k) { return dd_le(k, x0); });
-                hh = (hh + d) & (WCAP - 1);
-                hc -= d;
-                // fill until a heavy key > xm is present
-                while ((hc == 0 || dd_le(S.HK[(hh + hc - 1) & (WCAP - 1)], xm)) && gh < G &&
-                       hc + CH <= WCAP) {
-                    if (hc == 0) gh = seek_chunk<false>(W, gh, G, x0);
-                    if (gh >= G) break;
-                    hc += append_chunk<T, false>(w, n, avg, W, gh, S.HK, S.HI, hh + hc, lane);
-                    ++gh;
-                }
-                u32 r1;
-                if (hc == 0) {
-                    r1 = nl;  // no heavy key past these lights: own rows
-                    for (u32 r = r0 + lane; r < r1; r += 32) {
-                        const u32 pos = S.OP[r];
-                        S.RW[pos].alias = (AliasT)(cb + pos + 1);
-                    }
-                } else {
-                    const dd last = S.HK[(hh + hc - 1) & (WCAP - 1)];
-                    r1 = nl;
-                    if (!dd_lt(xm, last)) {  // window ends inside this chunk's lights
-                        u32 a = r0, b = nl;
-                        while (a < b) {
-                            const u32 mid = (a + b) >> 1;
-                            if (dd_lt(S.OK[mid], last)) a = mid + 1;
-                            else b = mid;
-                        }
-                        r1 = a;
-                        if (gh >= G) r1 = nl;  // nothing left to append: the rest have no heavy past them
-                    }
-                    for (u32 r = r0 + lane; r < r1; r += 32) {
-                        const dd x = S.OK[r];
-                        const u32 i = ring_search(S.HK, hh, hc, [&](dd k) { return dd_le(k, x); });
-                        const u32 pos = S.OP[r];
-                        const u64 al = i < hc ? (u64)S.HI[(hh + i) & (WCAP - 1)] + 1 : cb + pos + 1;
-                        S.RW[pos].alias = (AliasT)al;
-                    }
-                }
-                __syncwarp();
-                r0 = r1;
-            }
-            // ---- heavies: tw = key - (first light key >= heavy key) + avg
-            for (u32 r0 = 0; r0 < nh;) {
-                const dd y0 = S.OK[nl + r0], ym = S.OK[nl + nh - 1];
-                const u32 d = ring_search(S.LK, lh, lc, [&](dd k) { return dd_lt(k, y0); });
-                lh = (lh + d) & (WCAP - 1);
-                lc -= d;
-                while ((lc == 0 || dd_lt(S.LK[(lh + lc - 1) & (WCAP - 1)], ym)) && gl < G &&
-                       lc + CH <= WCAP) {
-                    if (lc == 0) gl = seek_chunk<true>(W, gl, G, y0);
-                    if (gl >= G) break;
-                    lc += append_chunk<T, true>(w, n, avg, W, gl, S.LK, nullptr, lh + lc, lane);
-                    ++gl;
-                }
-                u32 r1 = nh;
-                if (lc > 0) {
-                    const dd last = S.LK[(lh + lc - 1) & (WCAP - 1)];
-                    if (dd_lt(last, ym) && gl < G) {  // window ends inside: resolve y <= last
-                        u32 a = r0, b = nh;
-                        while (a < b) {
-                            const u32 mid = (a + b) >> 1;
-                            if (dd_le(S.OK[nl + mid], last)) a = mid + 1;
-                            else b = mid;
-                        }
-                        r1 = a;
-                    }
-                }
-                for (u32 r = r0 + lane; r < r1; r += 32) {
-                    const dd y = S.OK[nl + r];
-                    const u32 i = ring_search(S.LK, lh, lc, [&](dd k) { return dd_lt(k, y); });
-                    const dd DL = i < lc ? S.LK[(lh + i) & (WCAP - 1)] : Dtot;
-                    const dd tw = dd_add_d(dd_sub(y, DL), avg);
-                    S.RW[S.OP[nl + r]].tw = tw_store<T>(tw.hi + tw.lo, avg);
-                }
-                __syncwarp();
-                r0 = r1;
-            }
-            __syncwarp();
-            // ---- store the chunk's rows (each lane its 8 consecutive rows)
-            const u64 i0 = cb + (u64)lane * VV;
-            if (i0 + VV <= n) {
-                const uint4 *src = reinterpret_cast<const uint4 *>(&S.RW[lane * VV]);
-                uint4 *dst = reinterpret_cast<uint4 *>(rows_out + i0);
-#pragma unroll
-                for (int q = 0; q < (int)(VV * sizeof(RowT) / 16); ++q) dst[q] = src[q];
-            } else {
-                for (int k = 0; k < VV; ++k)
-                    if (i0 + k < n) rows_out[i0 + k] = S.RW[lane * VV + k];
-            }
-            __syncwarp();
         }
+    }
+    __syncthreads();
+    // heavy aliases: the next heavy of the tile, else the first heavy after it
+    {
+        const u64 after = W.nextH[u];
+        for (u32 r = threadIdx.x; r < nH; r += TB) {
+            const u32 pos = P.OP[nL + r];
+            u64 a;
+            if (r + 1 < nH) a = tb + P.OP[nL + r + 1] + 1;
+            else a = (after == NONE64) ? tb + pos + 1 : after + 1;
+            P.RW[pos].alias = (AliasT)a;
+        }
+    }
+    // (b) resolve lights, then heavies
+    if (nL) resolve_class<T, true>(w, n, avg, W, P, u, tb, 0, nL);
+    if (nH) resolve_class<T, false>(w, n, avg, W, P, u, tb, nL, nH);
+    __syncthreads();
+    // (c) store the tile's rows: each lane its 8 consecutive rows
+    const u64 i0 = cbase + (u64)lane * VV;
+    const u32 p0 = wid * CH + lane * VV;
+    if (i0 + VV <= n) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(&P.RW[p0]);
+        uint4 *dst = reinterpret_cast<uint4 *>(rows_out + i0);
+#pragma unroll
+        for (int q = 0; q < (int)(VV * sizeof(RowT) / 16); ++q) dst[q] = src[q];
+    } else {
+        for (int k = 0; k < VV; ++k)
+            if (i0 + k < n) rows_out[i0 + k] = P.RW[p0 + k];
     }
 }
 
@@ -800,17 +982,10 @@ int run_build(const void *wv, u64 n, double total, void *rows, void *ws, cudaStr
     AK_LAUNCH_CHECK("k_build_scan");
     k_build_coarse<<<(unsigned)((W.nt + 1 + 255) / 256), 256, 0, st>>>(W, n);
     AK_LAUNCH_CHECK("k_build_coarse");
-    const size_t smem = sizeof(WarpSmem<T>) * PW;
+    const size_t smem = sizeof(PackSmem<T>);
     AK_CUDA_TRY(cudaFuncSetAttribute(k_build_pack<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-    int per_sm = 0;
-    AK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_build_pack<T>, PW * 32, smem));
-    if (per_sm < 1) per_sm = 1;
-    const u64 G = (n + CH - 1) / CH, nruns = (G + RUN - 1) / RUN;
-    u64 grid = (u64)ak_num_sms() * per_sm;
-    if (grid * PW > nruns) grid = (nruns + PW - 1) / PW;
-    k_build_pack<T><<<(unsigned)grid, PW * 32, smem, st>>>(w, n, avg, W, (typename RowOf<T>::type *)rows,
-                                                          W.counter + 1);
+    k_build_pack<T><<<(unsigned)W.nt, TB, smem, st>>>(w, n, avg, W, (typename RowOf<T>::type *)rows);
     AK_LAUNCH_CHECK("k_build_pack");
     return AK_OK;
 }
