@@ -643,45 +643,53 @@ __device__ void resolve_class(const T *__restrict__ w, u64 n, double avg, const 
         }
     }
     __syncthreads();
-    // ---- the run of foreign chunks needed by [x_min, x_max]
-    if (threadIdx.x == 0) {
-        const u32 a = target_of<ISL>(W, P.SB, fast, nslot, fT0, fT1, DLu, DHu, P.OK[ob]);
-        u32 b = target_of<ISL>(W, P.SB, fast, nslot, fT0, fT1, DLu, DHu, P.OK[ob + cnt - 1]);
+    // ---- the run of foreign chunks needed by [x_min, x_max] (warp 0)
+    if (wid == 0) {
+        u32 ta = 0, tb2 = 0;
+        if (lane < 2)
+            ta = target_of<ISL>(W, P.SB, fast, nslot, fT0, fT1, DLu, DHu,
+                                P.OK[ob + (lane ? cnt - 1 : 0)]);
+        const u32 a = __shfl_sync(0xffffffffu, ta, 0);
+        u32 b = __shfl_sync(0xffffffffu, ta, 1);
+        (void)tb2;
         u32 dense = 0, nf = 0;
+        const bool tail_none = b == TG_NONE;
         if (a != TG_NONE) {
-            bool tail_none = b == TG_NONE;
             if (tail_none) b = (u32)(nt * NW - 1);
-            if (b >= a && b - a + 1 <= (u32)MAXRUN) {
-                // foreign counts of the run
-                u32 off = 0;
-                for (u32 g = a; g <= b; ++g) {
-                    P.u.d.off[g - a] = off;
+            const u32 len = b >= a ? b - a + 1 : 0;
+            if (len >= 1 && len <= (u32)MAXRUN) {
+                // per-chunk foreign counts of the run, one lane per chunk
+                u32 c = 0;
+                if ((u32)lane < len) {
+                    const u32 g = a + lane;
                     const u64 cs = (u64)g * CH;
                     const u32 valid = (u32)(n - cs < (u64)CH ? n - cs : (u64)CH);
                     const u32 nlc = W.mcl[g];
-                    off += ISL ? valid - nlc : nlc;
+                    c = ISL ? valid - nlc : nlc;
                 }
-                P.u.d.off[b - a + 1] = off;
-                if (off <= (u32)FCAP) {
+                u32 tot;
+                const u32 ex = warp_excl_count(c, tot, lane);
+                if ((u32)lane <= len) P.u.d.off[lane] = (u32)lane < len ? ex : tot;
+                if (tot <= (u32)FCAP) {
                     dense = 1;
-                    nf = off;
-                    const u64 tb_ = b / NW;
-                    const int cb_ = (int)(b % NW);
-                    if (ISL) {
-                        P.sent_item = tail_none ? NONE64 : W.nextH[tb_];  // refined below
-                    } else {
-                        P.sent = tail_none ? dd_sub(W.DLb[nt], DHu)
-                                           : add_dd_d(Dn(tb_), W.mD[b]);
-                    }
-                    (void)cb_;
+                    nf = tot;
                 }
             }
-            if (tail_none) b = TG_NONE;
         }
-        P.gA = a;
-        P.gB = b;
-        P.dense = dense;
-        P.nf = nf;
+        if (dense) {
+            if (ISL) {
+                const u64 sa = tail_none ? NONE64 : next_heavy_after(W, b / NW, (int)(b % NW), lane);
+                if (lane == 0) P.sent_item = sa;
+            } else if (lane == 0) {
+                P.sent = tail_none ? dd_sub(W.DLb[nt], DHu) : add_dd_d(Dn(b / NW), W.mD[b]);
+            }
+        }
+        if (lane == 0) {
+            P.gA = a;
+            P.gB = tail_none ? TG_NONE : b;
+            P.dense = dense;
+            P.nf = nf;
+        }
     }
     __syncthreads();
     const u32 gA = P.gA, gB = P.gB;
@@ -702,10 +710,6 @@ __device__ void resolve_class(const T *__restrict__ w, u64 n, double avg, const 
     if (P.dense) {
         const u32 nf = P.nf;
         const u32 gEnd = gB == TG_NONE ? (u32)(nt * NW - 1) : gB;
-        if (ISL && gB != TG_NONE && wid == 0) {
-            const u64 sa = next_heavy_after(W, gB / NW, (int)(gB % NW), lane);
-            if (lane == 0) P.sent_item = sa;
-        }
         // rebuild the run's keys, into the own frame
         for (u32 g = gA + wid; g <= gEnd; g += NW) {
             const u64 t = g / NW;

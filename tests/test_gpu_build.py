@@ -29,14 +29,18 @@ def tau(n):
 
 
 def compare(t, w64, total, *, quad=False):
-    """(alias mismatches vs f64 Vose, vs quad Vose, max heavy gap / avg,
-    light-threshold exactness)"""
+    """(alias mismatches vs the f64 reference Vose, vs binary128 Vose, max
+    threshold gap / avg).  With quad=True the gap is taken against the
+    binary128 Vose (same decisions as the device at every size; the f64
+    reference's drift can move a heavy's closing point without changing its
+    alias, so its thresholds are not comparable row by row at large N)."""
     ref = O.vose_construct(w64, total)
     tw, al = t.to_numpy()
     avg = total / w64.size
     light = w64 <= avg
     am = int(np.count_nonzero(al != ref.alias))
     amq = None
+    base = ref
     if quad:
         q = O.vose_construct_quad(w64, total)
         amq = int(np.count_nonzero(al != q.alias))
@@ -44,8 +48,9 @@ def compare(t, w64, total, *, quad=False):
         drift = np.nonzero(ref.alias != q.alias)[0]
         ours = np.nonzero(al != ref.alias)[0]
         assert set(ours.tolist()) <= set(drift.tolist())
-    same = al == ref.alias
-    gap = float(np.max(np.abs(tw - ref.tw)[same])) / avg if same.any() else 0.0
+        base = q
+    same = al == base.alias
+    gap = float(np.max(np.abs(tw - base.tw)[same])) / avg if same.any() else 0.0
     if t.dtype == torch.float64:
         assert np.array_equal(tw[light], w64[light])
     else:
@@ -176,7 +181,7 @@ def test_large_n_against_reference(n, dist, dtype):
     assert amq == 0, f"{amq} rows differ from the drift-free sequential order"
     if n <= 10**6:
         assert am == 0
-    assert gap <= tau(n) if dtype == torch.float64 else gap <= 1e-6 + tau(n)
+    assert gap <= 1e-9 if dtype == torch.float64 else gap <= 1e-6
     rep = ak.validate_table(t, ws, tol=1e-9 if dtype == torch.float64 else 1e-4, row_tol=tau(n))
     assert rep.ok, rep
     print(f"N={n} {dist} {dtype}: alias vs f64 reference {am} (its drift flips), gap {gap:.2e}, {rep}")

@@ -284,7 +284,7 @@ def t_big():
         torch.cuda.synchronize()
         dt_s = time.time() - t0
         am, gap = table_cmp(t, ref.tw, ref.alias, ws.average, 1e-9)
-        rep = ak.validate_table(t, ws, tol=1e-4 if dt == torch.float32 else 1e-9)
+        rep = ak.validate_table(t, ws, tol=1e-4 if dt == torch.float32 else 1e-9, row_tol=20 * n * 2.0**-53)
         print(f"   n={n} kind={kind} {dt}: alias mismatches {am}, gap {gap:.2e}, {rep}, {dt_s*1e3:.1f} ms")
         assert rep.ok
 
