@@ -23,7 +23,7 @@
 // double difference of two tile bases is formed as a normalised double-double
 // and compared with a local key.
 //
-// Pipeline (three kernels):
+// Pipeline (four kernels):
 //  1. k_build_scan   one pass over the weights (128-bit loads): classify, chunk
 //                    scans, per-tile totals and chunk bounds; a single-pass
 //                    decoupled look-back over super-tiles (32 tiles per CTA,
@@ -34,12 +34,14 @@
 //                    the first heavy tile covering its light keys (T1) and
 //                    the first light tile covering its heavy keys (S1), and
 //                    the first heavy after it (nextH).
-//  3. k_build_pack   CTA per tile: rebuild the tile's keys (lights and heavies
-//                    key-sorted in shared memory); per class, rebuild the run
-//                    of foreign chunks its keys need (L2-resident: the
-//                    neighbouring CTAs own them) in the tile's own frame and
-//                    merge-path them against the own keys; rows staged in
-//                    shared memory and stored once, coalesced.
+//  3. k_build_split  PSA split: for every section (light tile) boundary, the
+//                    heavy rank J = #heavies with key <= DLb[u] (tile from the
+//                    coarse merge, chunk from the stored bounds, count from
+//                    one chunk's canonical keys).
+//  4. k_build_pack   CTA per section: the tile's lights and the heavies of
+//                    ranks [J(u), J(u+1)) (any tiles; L2-resident, being the
+//                    lights' neighbours in key space) are merged once by a
+//                    merge path; each row is written exactly once.
 //  DRAM traffic ~ read w twice + write the rows once = the algorithmic bytes.
 #include "ak_common.cuh"
 
@@ -122,11 +124,17 @@ inline BuildWs carve(void *ws, u64 n)
     return W;
 }
 
+size_t split_bytes(u64 n)
+{
+    const u64 nt = (n + TILE - 1) / TILE;
+    return align256(3 * (nt + 2) * 8);
+}
+
 size_t ws_bytes_for(u64 n)
 {
     size_t off = 0;
     layout(n, [&](int, size_t b) { off += align256(b); });
-    return off + 256;
+    return off + 256 + split_bytes(n);
 }
 
 // ---------------------------------------------------------------------------
@@ -472,49 +480,37 @@ __global__ void k_build_coarse(BuildWs W, u64 n)
     }
 }
 
-// ---------------------------------------------------------------------------
-// 3. tile pack: merge-path against the needed foreign chunks
-// ---------------------------------------------------------------------------
-// One CTA owns one tile (8 warps).  (a) The warps rebuild the tile's
-// canonical keys; lights and heavies are laid out key-sorted in shared
-// memory.  (b) Per class, the own keys [x_min, x_max] need a contiguous run
-// of foreign chunks of the other class (the chunk holding the first key past
-// x_min through the one holding the first key past x_max).  Dense path: the
-// warps rebuild those chunks' keys once, converted into the tile's own frame
-// (exact double-doubles), at offsets known from the pass-1 chunk counts; one
-// CTA-wide merge path then gives every own element its successor.  Sparse
-// path (the run is too long, e.g. next to a giant heavy): every own element
-// gets its target chunk, equal targets form groups, and a warp resolves each
-// group against its one chunk.  (c) The rows are stored once, coalesced.
-constexpr int MAXSLOT = 4;       // candidate foreign tiles with cached bounds
-constexpr int GCAP = 256;        // groups per round (sparse path)
-constexpr int FCAP = 1280;       // foreign keys per merge (dense path)
-constexpr int MAXRUN = 32;       // foreign chunks per merge (dense path)
-constexpr u32 TG_NONE = 0xFFFFFFFFu;
+__device__ __forceinline__ u32 warp_excl_count(u32 cnt, u32 &total, int lane)
+{
+    u32 inc = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        u32 a = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += a;
+    }
+    total = __shfl_sync(0xffffffffu, inc, 31);
+    return inc - cnt;
+}
 
-template <typename T> struct PackSmem {
-    double OK[TILE];                    // own keys (tile-local): lights [0,nL), heavies [nL,nL+nH)
-    typename RowOf<T>::type RW[TILE];   // staged rows
-    unsigned short OP[TILE];            // own item offsets
-    union {
-        struct {                        // dense path
-            dd FK[FCAP];                // foreign keys in the own frame
-            u32 FI[FCAP];               // foreign heavy items (0-based, low 32 bits)
-            u32 off[MAXRUN + 1];        // per-chunk offsets into FK
-        } d;
-        struct {                        // sparse path
-            double F[NW][CH];
-            u32 TG[TILE];
-            unsigned char FP[NW][CH];
-            u32 GT[GCAP];
-            unsigned short GS[GCAP + 1];
-        } s;
-    } u;
-    dd SB[MAXSLOT * NW];                // own-frame chunk bounds of the candidate tiles
-    dd sent;                            // dense sentinel key (lights: bound after the run)
-    u64 sent_item;                      // dense sentinel item (heavies: next heavy after the run)
-    u32 cnt[NW], cnt2[NW];
-    u32 gA, gB, dense, nf;
+// ---------------------------------------------------------------------------
+// 3. PSA split: heavy rank at every section boundary
+// ---------------------------------------------------------------------------
+// Sections are the light tiles: section u holds the lights of tile u and the
+// heavies whose keys fall in its light key range (DLb[u], DLb[u+1]].  Its
+// boundary is J(DLb[u]) = #heavies with key <= DLb[u] — the reference's
+// split (split.py:69-77: the greatest h with H[h] <= cap - L[n-h]).  One warp
+// per boundary: the tile T1[u] from the coarse merge, the chunk from the
+// pass-1 chunk bounds (8 lanes at once), the count inside the chunk from its
+// canonical keys.  Outputs: the boundary's heavy rank, the chunk holding that
+// rank, and the item of that heavy (the first heavy past the boundary).
+constexpr int HCAP = 1408;       // heavies per merge round
+constexpr int CB = 32;           // chunks enumerated per round
+constexpr u32 NONE32 = 0xFFFFFFFFu;
+
+struct SplitOut {
+    u64 *hrank;   // [nt+2]
+    u64 *hchunk;  // [nt+2]
+    u64 *hitem;   // [nt+2]
 };
 
 // d + x as a normalised double-double (exact for the key ranges in play)
@@ -527,12 +523,19 @@ __device__ __forceinline__ dd add_dd_d(dd d, double x)
     fast_two_sum(s, e, h, l);
     return dd_make(h, l);
 }
-// f <= X and f < X for normalised X (double vs double-double)
-__device__ __forceinline__ bool le_d_dd(double f, dd X) { return f < X.hi || (f == X.hi && X.lo >= 0.0); }
-__device__ __forceinline__ bool lt_d_dd(double f, dd X) { return f < X.hi || (f == X.hi && X.lo > 0.0); }
-// X <= f and X < f
+// X <= f for normalised X
 __device__ __forceinline__ bool le_dd_d(dd X, double f) { return X.hi < f || (X.hi == f && X.lo <= 0.0); }
-__device__ __forceinline__ bool lt_dd_d(dd X, double f) { return X.hi < f || (X.hi == f && X.lo < 0.0); }
+
+__device__ __forceinline__ u64 heavies_before_tile(const BuildWs &W, u64 n, u64 t)
+{
+    const u64 items = t * TILE < n ? t * TILE : n;
+    return items - W.kL[t];
+}
+__device__ __forceinline__ u32 chunk_valid(u64 n, u64 g)
+{
+    const u64 cs = g * CH;
+    return cs >= n ? 0u : (u32)(n - cs < (u64)CH ? n - cs : (u64)CH);
+}
 
 // first heavy item (0-based) after chunk c of tile t (NONE64 if none)
 __device__ __forceinline__ u64 next_heavy_after(const BuildWs &W, u64 t, int c, int lane)
@@ -547,430 +550,296 @@ __device__ __forceinline__ u64 next_heavy_after(const BuildWs &W, u64 t, int c, 
     return W.nextH[t];
 }
 
-// Canonical (tile-local) keys of one class of chunk (t, c) and their mask.
-template <typename T, bool LIGHT>
-__device__ __forceinline__ u32 chunk_keys(const T *__restrict__ w, u64 n, double avg,
-                                          const BuildWs &W, u64 t, int c, double k[VV], int lane)
+template <typename T>
+__global__ void __launch_bounds__(TB) k_build_split(const T *__restrict__ w, u64 n, double avg,
+                                                    BuildWs W, SplitOut O)
 {
-    const double *mB = LIGHT ? W.mD : W.mE;
-    const double base = c ? mB[t * NW + c - 1] : 0.0, bound = mB[t * NW + c];
-    double v[VV], ex, tot;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const u64 nt = W.nt;
+    const u64 b = (u64)blockIdx.x * NW + wid;  // boundary
+    if (b > nt) return;
+    const dd x = W.DLb[b];
+    const u64 t = W.T1[b];
+    const u64 nh = heavies_before_tile(W, n, nt);
+    if (t >= nt) {
+        if (lane == 0) {
+            O.hrank[b] = nh;
+            O.hchunk[b] = nt * NW;
+            O.hitem[b] = NONE64;
+        }
+        return;
+    }
+    const dd xr = dd_sub(x, W.DHb[t]);  // boundary in tile t's heavy frame
+    // first chunk whose heavy bound passes xr (chunks before are entirely <= x)
+    const double bnd = lane < NW ? W.mE[t * NW + lane] : 0.0;
+    const unsigned pm = __ballot_sync(0xffffffffu, lane < NW && !(dd_le(dd_make(bnd), xr)));
+    const int c = pm ? __ffs(pm) - 1 : NW - 1;
+    // heavies of tile t in chunks before c
+    u32 hc = 0;
+    if (lane < c) hc = chunk_valid(n, t * NW + lane) - W.mcl[t * NW + lane];
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) hc += __shfl_xor_sync(0xffffffffu, hc, d);
+    // canonical heavy keys of chunk (t, c): count those <= xr
+    const double base = c ? W.mE[t * NW + c - 1] : 0.0, bound = W.mE[t * NW + c];
+    double v[VV], k[VV], ex, tot;
     u32 m;
     load8(w, n, t * TILE + (u64)c * CH + (u64)lane * VV, v);
-    lane_class<LIGHT>(v, avg, k, m, ex, tot, lane);
+    lane_class<false>(v, avg, k, m, ex, tot, lane);
     class_keys(k, ex, base, bound, lane);
-    return m;
+    u32 le = 0;
+#pragma unroll
+    for (int q = 0; q < VV; ++q) le += ((m >> q) & 1) && dd_le(dd_make(k[q]), xr);
+    u32 cnt = __popc(m), allc = cnt, alle = le;
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        allc += __shfl_xor_sync(0xffffffffu, allc, d);
+        alle += __shfl_xor_sync(0xffffffffu, alle, d);
+    }
+    // item of the first heavy past x: the alle-th heavy of the chunk, or later
+    u64 item = NONE64;
+    if (alle < allc) {
+        // locate the (alle)-th heavy in lane order
+        u32 inc = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            u32 a = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += a;
+        }
+        const u32 exc = inc - cnt;
+        u64 mine = NONE64;
+        if (alle >= exc && alle < inc) {
+            u32 r = alle - exc, mm = m;
+            for (u32 s = 0; s < r; ++s) mm &= mm - 1;
+            mine = t * TILE + (u64)c * CH + (u64)lane * VV + (__ffs(mm) - 1);
+        }
+        unsigned own = __ballot_sync(0xffffffffu, mine != NONE64);
+        item = __shfl_sync(0xffffffffu, mine, __ffs(own) - 1);
+    } else {
+        item = next_heavy_after(W, t, c, lane);
+    }
+    if (lane == 0) {
+        O.hrank[b] = heavies_before_tile(W, n, t) + hc + alle;
+        O.hchunk[b] = t * NW + c;
+        O.hitem[b] = item;
+    }
 }
 
-__device__ __forceinline__ u32 warp_excl_count(u32 cnt, u32 &total, int lane)
-{
-    u32 inc = cnt;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        u32 a = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += a;
-    }
-    total = __shfl_sync(0xffffffffu, inc, 31);
-    return inc - cnt;
-}
-
-// Target chunk of own key x (tile-local, own frame): the foreign chunk of
-// the other class holding the first key past x (ISL: first heavy key > x;
-// else first light key >= x), TG_NONE if beyond every chunk.
-template <bool ISL>
-__device__ u32 target_of(const BuildWs &W, const dd *SB, bool fast, u32 nslot, u64 fT0, u64 fT1,
-                         dd DLu, dd DHu, double x)
-{
-    const u64 nt = W.nt;
-    if (fast) {
-        u32 a = 0, b = nslot * NW;
-        while (a < b) {
-            const u32 mid = (a + b) >> 1;
-            const bool before = ISL ? !lt_d_dd(x, SB[mid]) : !le_d_dd(x, SB[mid]);
-            if (before) a = mid + 1;
-            else b = mid;
-        }
-        if (a < nslot * NW) {
-            const u64 t = fT0 + a / NW;
-            return t < nt ? (u32)(t * NW + a % NW) : TG_NONE;
-        }
-        return TG_NONE;
-    }
-    u64 a = fT0, b = fT1 + 1;
-    while (a < b) {
-        const u64 mid = (a + b) >> 1;
-        bool before;
-        if (mid >= nt) before = false;
-        else {
-            const dd L = ISL ? dd_sub(W.DHb[mid + 1], DLu) : dd_sub(W.DLb[mid + 1], DHu);
-            before = ISL ? !lt_d_dd(x, L) : !le_d_dd(x, L);
-        }
-        if (before) a = mid + 1;
-        else b = mid;
-    }
-    if (a > fT1 || a >= nt) return TG_NONE;
-    const dd D = ISL ? dd_sub(W.DHb[a], DLu) : dd_sub(W.DLb[a], DHu);  // foreign base - own base
-    const double *mB = (ISL ? W.mE : W.mD) + a * NW;
-    int c = 0;
-    for (; c < NW - 1; ++c) {
-        const dd B = add_dd_d(D, mB[c]);
-        if (ISL ? lt_d_dd(x, B) : le_d_dd(x, B)) break;
-    }
-    return (u32)(a * NW + c);
-}
-
-template <typename T, bool ISL>
-__device__ void resolve_class(const T *__restrict__ w, u64 n, double avg, const BuildWs &W,
-                              PackSmem<T> &P, u64 u, u64 tb, u32 ob, u32 cnt)
-{
-    typedef typename RowOf<T>::type RowT;
-    typedef decltype(RowT::alias) AliasT;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const u64 nt = W.nt;
-    const dd DLu = W.DLb[u], DHu = W.DHb[u];
-    const dd own_base = ISL ? DLu : DHu;
-    const u64 fT0 = ISL ? W.T1[u] : W.S1[u];
-    const u64 fT1 = ISL ? W.T1[u + 1] : W.S1[u + 1];
-    // foreign base - own base: a foreign local key f is f + Dn in the own frame
-    auto Dn = [&](u64 t) -> dd { return dd_sub(ISL ? W.DHb[t] : W.DLb[t], own_base); };
-    const bool fast = fT1 - fT0 + 1 <= (u64)MAXSLOT;
-    const u32 nslot = fast ? (u32)(fT1 - fT0 + 1) : 0;
-    if (fast) {
-        for (u32 i = threadIdx.x; i < nslot * NW; i += TB) {
-            const u64 t = fT0 + i / NW;
-            P.SB[i] = t >= nt ? dd_make(INFINITY, 0.0)
-                              : add_dd_d(Dn(t), (ISL ? W.mE : W.mD)[t * NW + i % NW]);
-        }
-    }
-    __syncthreads();
-    // ---- the run of foreign chunks needed by [x_min, x_max] (warp 0)
-    if (wid == 0) {
-        u32 ta = 0, tb2 = 0;
-        if (lane < 2)
-            ta = target_of<ISL>(W, P.SB, fast, nslot, fT0, fT1, DLu, DHu,
-                                P.OK[ob + (lane ? cnt - 1 : 0)]);
-        const u32 a = __shfl_sync(0xffffffffu, ta, 0);
-        u32 b = __shfl_sync(0xffffffffu, ta, 1);
-        (void)tb2;
-        u32 dense = 0, nf = 0;
-        const bool tail_none = b == TG_NONE;
-        if (a != TG_NONE) {
-            if (tail_none) b = (u32)(nt * NW - 1);
-            const u32 len = b >= a ? b - a + 1 : 0;
-            if (len >= 1 && len <= (u32)MAXRUN) {
-                // per-chunk foreign counts of the run, one lane per chunk
-                u32 c = 0;
-                if ((u32)lane < len) {
-                    const u32 g = a + lane;
-                    const u64 cs = (u64)g * CH;
-                    const u32 valid = (u32)(n - cs < (u64)CH ? n - cs : (u64)CH);
-                    const u32 nlc = W.mcl[g];
-                    c = ISL ? valid - nlc : nlc;
-                }
-                u32 tot;
-                const u32 ex = warp_excl_count(c, tot, lane);
-                if ((u32)lane <= len) P.u.d.off[lane] = (u32)lane < len ? ex : tot;
-                if (tot <= (u32)FCAP) {
-                    dense = 1;
-                    nf = tot;
-                }
-            }
-        }
-        if (dense) {
-            if (ISL) {
-                const u64 sa = tail_none ? NONE64 : next_heavy_after(W, b / NW, (int)(b % NW), lane);
-                if (lane == 0) P.sent_item = sa;
-            } else if (lane == 0) {
-                P.sent = tail_none ? dd_sub(W.DLb[nt], DHu) : add_dd_d(Dn(b / NW), W.mD[b]);
-            }
-        }
-        if (lane == 0) {
-            P.gA = a;
-            P.gB = tail_none ? TG_NONE : b;
-            P.dense = dense;
-            P.nf = nf;
-        }
-    }
-    __syncthreads();
-    const u32 gA = P.gA, gB = P.gB;
-    if (gA == TG_NONE) {
-        // no foreign key past any own key
-        for (u32 r = threadIdx.x; r < cnt; r += TB) {
-            const u32 pos = P.OP[ob + r];
-            if (ISL) {
-                P.RW[pos].alias = (AliasT)(tb + pos + 1);
-            } else {
-                const dd tw = dd_add_d(add_dd_d(dd_neg(dd_sub(W.DLb[nt], DHu)), P.OK[ob + r]), avg);
-                P.RW[pos].tw = tw_store<T>(tw.hi + tw.lo, avg);
-            }
-        }
-        __syncthreads();
-        return;
-    }
-    if (P.dense) {
-        const u32 nf = P.nf;
-        const u32 gEnd = gB == TG_NONE ? (u32)(nt * NW - 1) : gB;
-        // rebuild the run's keys, into the own frame
-        for (u32 g = gA + wid; g <= gEnd; g += NW) {
-            const u64 t = g / NW;
-            const int c = (int)(g % NW);
-            double k[VV];
-            const u32 m = chunk_keys<T, !ISL>(w, n, avg, W, t, c, k, lane);
-            u32 tot;
-            u32 r = P.u.d.off[g - gA] + warp_excl_count(__popc(m), tot, lane);
-            const dd D = Dn(t);
-#pragma unroll
-            for (int q = 0; q < VV; ++q)
-                if ((m >> q) & 1) {
-                    P.u.d.FK[r] = add_dd_d(D, k[q]);
-                    if (ISL) P.u.d.FI[r] = (u32)((u64)g * CH + lane * VV + q);
-                    ++r;
-                }
-        }
-        __syncthreads();
-        // merge path: own [0,cnt) with foreign [0,nf); foreign first when
-        //   ISL: F <= x (heavy closes before the light);  else F < y
-        const u32 total = cnt + nf;
-        const u32 per = (total + TB - 1) / TB;
-        const u32 d0 = threadIdx.x * per;
-        if (d0 < total) {
-            u32 lo = d0 > nf ? d0 - nf : 0, hi = d0 < cnt ? d0 : cnt;
-            while (lo < hi) {
-                const u32 mid = (lo + hi) >> 1;
-                const u32 j = d0 - mid - 1;  // own[mid] precedes foreign[j]?
-                const dd Fj = P.u.d.FK[j];
-                const bool own_first = ISL ? !le_dd_d(Fj, P.OK[ob + mid]) : !lt_dd_d(Fj, P.OK[ob + mid]);
-                if (own_first) lo = mid + 1;
-                else hi = mid;
-            }
-            u32 i = lo, j = d0 - lo;
-            const u32 d1 = d0 + per < total ? d0 + per : total;
-            for (u32 d = d0; d < d1; ++d) {
-                bool take_own;
-                if (i >= cnt) take_own = false;
-                else if (j >= nf) take_own = true;
-                else {
-                    const dd Fj = P.u.d.FK[j];
-                    take_own = ISL ? !le_dd_d(Fj, P.OK[ob + i]) : !lt_dd_d(Fj, P.OK[ob + i]);
-                }
-                if (!take_own) {
-                    ++j;
-                    continue;
-                }
-                const u32 pos = P.OP[ob + i];
-                if (ISL) {
-                    u64 al;
-                    if (j < nf) al = (u64)P.u.d.FI[j] + 1;
-                    else al = P.sent_item == NONE64 ? tb + pos + 1 : P.sent_item + 1;
-                    P.RW[pos].alias = (AliasT)al;
-                } else {
-                    const dd DL = j < nf ? P.u.d.FK[j] : P.sent;
-                    const dd tw = dd_add_d(add_dd_d(dd_neg(DL), P.OK[ob + i]), avg);
-                    P.RW[pos].tw = tw_store<T>(tw.hi + tw.lo, avg);
-                }
-                ++i;
-            }
-        }
-        __syncthreads();
-        return;
-    }
-    // ---- sparse path: per-element targets, grouped
-    for (u32 i = threadIdx.x; i < cnt; i += TB)
-        P.u.s.TG[i] = target_of<ISL>(W, P.SB, fast, nslot, fT0, fT1, DLu, DHu, P.OK[ob + i]);
-    __syncthreads();
-    u32 e0 = 0;
-    while (e0 < cnt) {
-        const u32 per = (cnt - e0 + TB - 1) / TB;
-        const u32 i0 = e0 + threadIdx.x * per, i1 = min(i0 + per, cnt);
-        u32 nst = 0;
-        for (u32 i = i0; i < i1; ++i) nst += (i == e0 || P.u.s.TG[i] != P.u.s.TG[i - 1]);
-        u32 wt;
-        const u32 ex = warp_excl_count(nst, wt, lane);
-        if (lane == 0) P.cnt2[wid] = wt;
-        __syncthreads();
-        u32 wbase = 0, tot = 0;
-        for (int k = 0; k < NW; ++k) {
-            wbase += k < wid ? P.cnt2[k] : 0;
-            tot += P.cnt2[k];
-        }
-        u32 g = wbase + ex;
-        for (u32 i = i0; i < i1; ++i)
-            if (i == e0 || P.u.s.TG[i] != P.u.s.TG[i - 1]) {
-                if (g < GCAP) {
-                    P.u.s.GS[g] = (unsigned short)i;
-                    P.u.s.GT[g] = P.u.s.TG[i];
-                }
-                ++g;
-            }
-        __syncthreads();
-        const u32 ngr = tot <= GCAP ? tot : GCAP - 1;
-        const u32 e1 = tot <= GCAP ? cnt : P.u.s.GS[GCAP - 1];
-        __syncthreads();
-        if (threadIdx.x == 0) P.u.s.GS[ngr] = (unsigned short)e1;
-        __syncthreads();
-        for (u32 gi = wid; gi < ngr; gi += NW) {
-            const u32 ga = P.u.s.GS[gi], gb = P.u.s.GS[gi + 1];
-            const u32 tgt = P.u.s.GT[gi];
-            if (tgt == TG_NONE) {
-                for (u32 r = ga + lane; r < gb; r += 32) {
-                    const u32 pos = P.OP[ob + r];
-                    if (ISL) {
-                        P.RW[pos].alias = (AliasT)(tb + pos + 1);
-                    } else {
-                        const dd tw = dd_add_d(add_dd_d(dd_neg(dd_sub(W.DLb[nt], DHu)), P.OK[ob + r]), avg);
-                        P.RW[pos].tw = tw_store<T>(tw.hi + tw.lo, avg);
-                    }
-                }
-                continue;
-            }
-            const u64 t = tgt / NW;
-            const int c = (int)(tgt % NW);
-            double *F = P.u.s.F[wid];
-            unsigned char *FP = P.u.s.FP[wid];
-            double k[VV];
-            const u32 m = chunk_keys<T, !ISL>(w, n, avg, W, t, c, k, lane);
-            u32 nF;
-            u32 r = warp_excl_count(__popc(m), nF, lane);
-            __syncwarp();
-#pragma unroll
-            for (int q = 0; q < VV; ++q)
-                if ((m >> q) & 1) {
-                    F[r] = k[q];
-                    FP[r] = (unsigned char)(lane * VV + q);
-                    ++r;
-                }
-            __syncwarp();
-            const dd Do = dd_neg(Dn(t));  // own frame -> foreign frame: x - Dn
-            if (ISL) {
-                const u64 after = next_heavy_after(W, t, c, lane);
-                const u64 fb = t * TILE + (u64)c * CH;
-                for (u32 r2 = ga + lane; r2 < gb; r2 += 32) {
-                    const dd X = add_dd_d(Do, P.OK[ob + r2]);
-                    u32 a = 0, b = nF;  // first heavy key > X
-                    while (a < b) {
-                        const u32 mid = (a + b) >> 1;
-                        if (le_d_dd(F[mid], X)) a = mid + 1;
-                        else b = mid;
-                    }
-                    const u32 pos = P.OP[ob + r2];
-                    u64 al;
-                    if (a < nF) al = fb + FP[a] + 1;
-                    else al = (after == NONE64) ? tb + pos + 1 : after + 1;
-                    P.RW[pos].alias = (AliasT)al;
-                }
-            } else {
-                const double bound = W.mD[t * NW + c];
-                for (u32 r2 = ga + lane; r2 < gb; r2 += 32) {
-                    const dd Y = add_dd_d(Do, P.OK[ob + r2]);
-                    u32 a = 0, b = nF;  // first light key >= Y
-                    while (a < b) {
-                        const u32 mid = (a + b) >> 1;
-                        if (lt_d_dd(F[mid], Y)) a = mid + 1;
-                        else b = mid;
-                    }
-                    const double DL = a < nF ? F[a] : bound;
-                    const dd tw = dd_add_d(add_dd_d(Y, -DL), avg);
-                    P.RW[P.OP[ob + r2]].tw = tw_store<T>(tw.hi + tw.lo, avg);
-                }
-            }
-            __syncwarp();
-        }
-        __syncthreads();
-        e0 = e1;
-    }
-}
+// ---------------------------------------------------------------------------
+// 4. section pack: merge the section's lights with its heavies
+// ---------------------------------------------------------------------------
+// CTA u = section u.  Lights: the 8 chunks of tile u, canonical keys in the
+// tile's own frame (exact doubles).  Heavies: ranks [J(u), J(u+1)), rebuilt
+// chunk by chunk (any tile) and converted to the own frame (exact
+// double-doubles).  One merge path (heavy first on ties: DH <= DL) gives each
+// light its successor heavy and each heavy its successor light; rows are
+// written directly: lights by the threads that own them, heavies in rank
+// order.  Large heavy ranges are processed in rounds of HCAP.
+template <typename T> struct SecSmem {
+    double LK[TILE];               // own light keys (own frame), rank order
+    dd HK[HCAP];                   // heavy keys (own frame)
+    u32 HI[HCAP];                  // heavy items
+    u32 LS[TILE];                  // light successor item (+1), 0 = unresolved
+    unsigned short SL[HCAP];       // heavy -> successor light index
+    u64 cbase[CB + 1];             // heavy rank of each enumerated chunk's first heavy
+    u32 lcnt[NW];
+    u32 lfirst;
+    u64 next_item;                 // item of the heavy ranked jend (first of the next round)
+};
 
 template <typename T>
-__global__ void __launch_bounds__(TB, 3) k_build_pack(const T *__restrict__ w, u64 n, double avg,
-                                                      BuildWs W,
-                                                      typename RowOf<T>::type *__restrict__ rows_out)
+__global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u64 n, double avg,
+                                                      BuildWs W, SplitOut O,
+                                                      typename RowOf<T>::type *__restrict__ rows)
 {
     typedef typename RowOf<T>::type RowT;
+    typedef decltype(RowT::tw) TwT;
     typedef decltype(RowT::alias) AliasT;
-    extern __shared__ __align__(16) unsigned char pack_smem[];
-    PackSmem<T> &P = *reinterpret_cast<PackSmem<T> *>(pack_smem);
+    extern __shared__ __align__(16) unsigned char sec_smem[];
+    SecSmem<T> &P = *reinterpret_cast<SecSmem<T> *>(sec_smem);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const u64 u = blockIdx.x;
-    const u64 tb = u * TILE;
-    const u64 cbase = tb + (u64)wid * CH;
+    const u64 nt = W.nt;
+    const u64 u = blockIdx.x;  // section; u == nt: the heavies past every light
+    const u64 J0 = O.hrank[u], J1 = u < nt ? O.hrank[u + 1] : heavies_before_tile(W, n, nt);
+    const u64 after = u < nt ? O.hitem[u + 1] : NONE64;  // first heavy past the section
+    const dd own = u < nt ? W.DLb[u] : W.DLb[nt];
+    const double secbound = u < nt ? W.mD[u * NW + NW - 1] : 0.0;  // next light key, own frame
 
-    // (a) own tile: classify, counts, then canonical keys into sorted lists
-    double v[VV];
-    load8(w, n, cbase + (u64)lane * VV, v);
-    u32 lm = 0, hm = 0;
+    // ---- lights of tile u (rank order = key order)
+    u32 nL = 0, lrank0 = 0, lm = 0;
+    double lk[VV], lv[VV];
+    if (u < nt) {
+        if (lane == 0) P.lcnt[wid] = W.mcl[u * NW + wid];
+        load8(w, n, u * TILE + (u64)wid * CH + (u64)lane * VV, lv);
+        const double b0 = wid ? W.mD[u * NW + wid - 1] : 0.0, b1 = W.mD[u * NW + wid];
+        double ex, tot;
+        lane_class<true>(lv, avg, lk, lm, ex, tot, lane);
+        class_keys(lk, ex, b0, b1, lane);
+        u32 tl;
+        const u32 el = warp_excl_count(__popc(lm), tl, lane);
+        __syncthreads();
+        u32 woff = 0;
+        for (int k = 0; k < NW; ++k) {
+            woff += k < wid ? P.lcnt[k] : 0;
+            nL += P.lcnt[k];
+        }
+        lrank0 = woff + el;
+        u32 r = lrank0;
 #pragma unroll
-    for (int k = 0; k < VV; ++k) {
-        lm |= (u32)(v[k] >= 0.0 && v[k] <= avg) << k;
-        hm |= (u32)(v[k] > avg) << k;
-    }
-    u32 wl, wh;
-    const u32 el = warp_excl_count(__popc(lm), wl, lane);
-    const u32 eh = warp_excl_count(__popc(hm), wh, lane);
-    if (lane == 0) {
-        P.cnt[wid] = wl;
-        P.cnt2[wid] = wh;
+        for (int q = 0; q < VV; ++q)
+            if ((lm >> q) & 1) {
+                P.LK[r] = lk[q];
+                P.LS[r] = 0;
+                ++r;
+            }
     }
     __syncthreads();
-    u32 offL = 0, offH = 0, nL = 0, nH = 0;
-#pragma unroll
-    for (int k = 0; k < NW; ++k) {
-        offL += k < wid ? P.cnt[k] : 0;
-        offH += k < wid ? P.cnt2[k] : 0;
-        nL += P.cnt[k];
-        nH += P.cnt2[k];
-    }
-    {
-        const double bD0 = wid ? W.mD[u * NW + wid - 1] : 0.0, bD1 = W.mD[u * NW + wid];
-        const double bE0 = wid ? W.mE[u * NW + wid - 1] : 0.0, bE1 = W.mE[u * NW + wid];
-        double kD[VV], kE[VV], exD, exE, tD, tE;
-        u32 m1, m2;
-        lane_class<true>(v, avg, kD, m1, exD, tD, lane);
-        class_keys(kD, exD, bD0, bD1, lane);
-        lane_class<false>(v, avg, kE, m2, exE, tE, lane);
-        class_keys(kE, exE, bE0, bE1, lane);
-        u32 rl = offL + el, rh = nL + offH + eh;
-#pragma unroll
-        for (int k = 0; k < VV; ++k) {
-            const u32 pos = wid * CH + lane * VV + k;
-            if ((lm >> k) & 1) {
-                P.OK[rl] = kD[k];
-                P.OP[rl] = (unsigned short)pos;
-                P.RW[pos].tw = (decltype(RowT::tw))v[k];
-                ++rl;
-            } else if ((hm >> k) & 1) {
-                P.OK[rh] = kE[k];
-                P.OP[rh] = (unsigned short)pos;
-                ++rh;
+
+    // ---- heavies in rounds of at most HCAP ranks
+    u64 jcur = J0;
+    u64 gcur = O.hchunk[u];
+    u32 lfirst = 0;  // first light not yet resolved
+    while (jcur < J1) {
+        // enumerate CB chunks from gcur with the heavy rank of their first heavy
+        if (wid == 0) {
+            const u64 g = gcur + lane;
+            u64 hb = ~0ull;
+            u32 hcnt = 0;
+            if (g < nt * NW) {
+                const u64 t = g / NW;
+                const int c = (int)(g % NW);
+                hcnt = chunk_valid(n, g) - W.mcl[g];
+                u32 pre = 0;
+                for (int k = 0; k < c; ++k) pre += chunk_valid(n, t * NW + k) - W.mcl[t * NW + k];
+                hb = heavies_before_tile(W, n, t) + pre;
+            }
+            P.cbase[lane] = hb;
+            const u64 last = __shfl_sync(0xffffffffu, hb == ~0ull ? ~0ull : hb + hcnt, 31);
+            if (lane == 0) {
+                P.cbase[CB] = last;
+                P.next_item = NONE64;
             }
         }
-    }
-    __syncthreads();
-    // heavy aliases: the next heavy of the tile, else the first heavy after it
-    {
-        const u64 after = W.nextH[u];
-        for (u32 r = threadIdx.x; r < nH; r += TB) {
-            const u32 pos = P.OP[nL + r];
-            u64 a;
-            if (r + 1 < nH) a = tb + P.OP[nL + r + 1] + 1;
-            else a = (after == NONE64) ? tb + pos + 1 : after + 1;
-            P.RW[pos].alias = (AliasT)a;
-        }
-    }
-    // (b) resolve lights, then heavies
-    if (nL) resolve_class<T, true>(w, n, avg, W, P, u, tb, 0, nL);
-    if (nH) resolve_class<T, false>(w, n, avg, W, P, u, tb, nL, nH);
-    __syncthreads();
-    // (c) store the tile's rows: each lane its 8 consecutive rows
-    const u64 i0 = cbase + (u64)lane * VV;
-    const u32 p0 = wid * CH + lane * VV;
-    if (i0 + VV <= n) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(&P.RW[p0]);
-        uint4 *dst = reinterpret_cast<uint4 *>(rows_out + i0);
+        __syncthreads();
+        u64 jend = J1 < jcur + HCAP ? J1 : jcur + HCAP;
+        if (P.cbase[CB] < jend) jend = P.cbase[CB];
+        const u32 nH = (u32)(jend - jcur);
+        const bool last_round = jend >= J1;
+        // rebuild the chunks covering ranks [jcur, jend], own frame
+        for (int ci = wid; ci < CB; ci += NW) {
+            const u64 hb = P.cbase[ci], hn = P.cbase[ci + 1];
+            if (hb == ~0ull || hb > jend || hn <= jcur) continue;
+            const u64 g = gcur + ci;
+            const u64 t = g / NW;
+            const int c = (int)(g % NW);
+            const double base = c ? W.mE[g - 1] : 0.0, bound = W.mE[g];
+            const dd D = dd_sub(W.DHb[t], own);
+            double v[VV], k[VV], ex, tot;
+            u32 m;
+            load8(w, n, g * CH + (u64)lane * VV, v);
+            lane_class<false>(v, avg, k, m, ex, tot, lane);
+            class_keys(k, ex, base, bound, lane);
+            u32 tc;
+            u64 rr = hb + warp_excl_count(__popc(m), tc, lane);
 #pragma unroll
-        for (int q = 0; q < (int)(VV * sizeof(RowT) / 16); ++q) dst[q] = src[q];
-    } else {
-        for (int k = 0; k < VV; ++k)
-            if (i0 + k < n) rows_out[i0 + k] = P.RW[p0 + k];
+            for (int q = 0; q < VV; ++q)
+                if ((m >> q) & 1) {
+                    const u32 item = (u32)(g * CH + (u64)lane * VV + q);
+                    if (rr >= jcur && rr < jend) {
+                        const u32 s = (u32)(rr - jcur);
+                        P.HK[s] = add_dd_d(D, k[q]);
+                        P.HI[s] = item;
+                    } else if (rr == jend) {
+                        P.next_item = item;
+                    }
+                    ++rr;
+                }
+        }
+        __syncthreads();
+        if (!last_round && wid == 0 && P.next_item == NONE64) {
+            // rank jend lies past the enumerated chunks
+            const u64 gl = gcur + CB - 1;
+            const u64 nx = next_heavy_after(W, gl / NW, (int)(gl % NW), lane);
+            if (lane == 0) P.next_item = nx;
+        }
+        // merge path: lights [lfirst, nL) with heavies [0, nH); heavy first on ties
+        {
+            const u32 na = nL - lfirst;
+            const u32 total = na + nH;
+            const u32 per = (total + TB - 1) / TB;
+            const u32 d0 = threadIdx.x * per;
+            if (d0 < total) {
+                u32 lo = d0 > nH ? d0 - nH : 0, hi = d0 < na ? d0 : na;
+                while (lo < hi) {
+                    const u32 mid = (lo + hi) >> 1;
+                    if (!le_dd_d(P.HK[d0 - mid - 1], P.LK[lfirst + mid])) lo = mid + 1;
+                    else hi = mid;
+                }
+                u32 i = lo, j = d0 - lo;
+                const u32 d1 = d0 + per < total ? d0 + per : total;
+                for (u32 d = d0; d < d1; ++d) {
+                    const bool light = i < na && (j >= nH || !le_dd_d(P.HK[j], P.LK[lfirst + i]));
+                    if (light) {
+                        if (j < nH) P.LS[lfirst + i] = P.HI[j] + 1;
+                        ++i;
+                    } else {
+                        P.SL[j] = (unsigned short)(lfirst + i);
+                        ++j;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // heavy rows of this round
+        const u64 nxt = last_round ? after : P.next_item;
+        for (u32 j = threadIdx.x; j < nH; j += TB) {
+            const u32 item = P.HI[j];
+            const u32 sl = P.SL[j];
+            const double DL = sl < nL ? P.LK[sl] : secbound;
+            const dd tw = dd_add_d(add_dd_d(P.HK[j], -DL), avg);
+            u64 al;
+            if (j + 1 < nH) al = (u64)P.HI[j + 1] + 1;
+            else al = nxt == NONE64 ? (u64)item + 1 : nxt + 1;
+            RowT row;
+            row.tw = tw_store<T>(tw.hi + tw.lo, avg);
+            row.alias = (AliasT)al;
+            rows[item] = row;
+        }
+        // the resolved lights form a prefix: the next round starts after it
+        if (!last_round && threadIdx.x == 0) {
+            u32 a = lfirst, b = nL;
+            while (a < b) {
+                const u32 mid = (a + b) >> 1;
+                if (P.LS[mid] != 0) a = mid + 1;
+                else b = mid;
+            }
+            P.lfirst = a;
+        }
+        u64 gnext = gcur;
+        for (int ci = 0; ci < CB; ++ci) {
+            const u64 hb = P.cbase[ci];
+            if (hb != ~0ull && hb <= jend) gnext = gcur + ci;
+        }
+        __syncthreads();
+        if (!last_round) lfirst = P.lfirst;
+        gcur = gnext;
+        jcur = jend;
+    }
+    // lights: rows written by their owning lanes; unresolved ones alias the
+    // first heavy past the section (or themselves)
+    if (u < nt) {
+        u32 r = lrank0;
+#pragma unroll
+        for (int q = 0; q < VV; ++q)
+            if ((lm >> q) & 1) {
+                const u64 item = u * TILE + (u64)wid * CH + (u64)lane * VV + q;
+                const u32 s = P.LS[r];
+                const u64 al = s ? (u64)s : (after == NONE64 ? item + 1 : after + 1);
+                RowT row;
+                row.tw = (TwT)lv[q];
+                row.alias = (AliasT)al;
+                rows[item] = row;
+                ++r;
+            }
     }
 }
 
@@ -980,16 +849,26 @@ int run_build(const void *wv, u64 n, double total, void *rows, void *ws, cudaStr
     const T *w = (const T *)wv;
     BuildWs W = carve(ws, n);
     const double avg = total / (double)n;
+    SplitOut O;
+    {
+        char *tail = (char *)ws + ws_bytes_for(n) - split_bytes(n);
+        O.hrank = (u64 *)tail;
+        O.hchunk = O.hrank + (W.nt + 2);
+        O.hitem = O.hchunk + (W.nt + 2);
+    }
     AK_CUDA_TRY(cudaMemsetAsync(W.counter, 0, 256, st));
     AK_CUDA_TRY(cudaMemsetAsync(W.status, 0, W.nst * 4, st));
     k_build_scan<T><<<(unsigned)W.nst, TB, 0, st>>>(w, n, avg, W);
     AK_LAUNCH_CHECK("k_build_scan");
     k_build_coarse<<<(unsigned)((W.nt + 1 + 255) / 256), 256, 0, st>>>(W, n);
     AK_LAUNCH_CHECK("k_build_coarse");
-    const size_t smem = sizeof(PackSmem<T>);
+    k_build_split<T><<<(unsigned)((W.nt + 1 + NW - 1) / NW), TB, 0, st>>>(w, n, avg, W, O);
+    AK_LAUNCH_CHECK("k_build_split");
+    const size_t smem = sizeof(SecSmem<T>);
     AK_CUDA_TRY(cudaFuncSetAttribute(k_build_pack<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-    k_build_pack<T><<<(unsigned)W.nt, TB, smem, st>>>(w, n, avg, W, (typename RowOf<T>::type *)rows);
+    k_build_pack<T><<<(unsigned)(W.nt + 1), TB, smem, st>>>(w, n, avg, W, O,
+                                                           (typename RowOf<T>::type *)rows);
     AK_LAUNCH_CHECK("k_build_pack");
     return AK_OK;
 }
