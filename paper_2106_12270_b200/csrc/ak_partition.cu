@@ -342,9 +342,12 @@ __global__ void __launch_bounds__(PLAN_RUN) k_plan_batched(PlanArgs A, const T *
     __syncthreads();
     const i64 hA = ends[0], hB = ends[1];
     const i64 nA = boundary_n(i0, A.n_total, A.s), nB = boundary_n(i1, A.n_total, A.s);
-    // windows: H[hA .. hB], L[nA - hB .. nB - hA]
+    // windows: H[hA .. hB], L[nA - hB .. nB - hA] clipped to [0, nl] (every
+    // probe ni - h of the searches below lies in that range)
     const i64 hlen = hB - hA + 1;
-    const i64 l0 = nA - hB, llen = (nB - hA) - l0 + 1;
+    const i64 l0 = nA - hB > 0 ? nA - hB : 0;
+    const i64 l1 = nB - hA < A.nl ? nB - hA : A.nl;
+    const i64 llen = l1 - l0 + 1;
     const bool staged = hlen > 0 && llen > 0 && hlen + llen <= PLAN_SMEM_DOUBLES;
     if (staged) {
         for (i64 t = threadIdx.x; t < hlen; t += blockDim.x) stage[t] = A.hpre[hA + t];

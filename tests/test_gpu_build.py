@@ -86,9 +86,10 @@ def test_golden_cases_alias_exact(golden):
         tw, al = t.to_numpy()
         diff = np.nonzero(al != golden[k + "vose_alias"])[0] + 1
         if ci % 5 == 3:
-            ref_self = max(int(np.count_nonzero(golden[k + f"psa{s}_alias"] != golden[k + "vose_alias"]))
-                           for s in (2, 7, 64) if s <= w.size)
-            assert diff.size <= max(8, 2 * ref_self), (diff.size, ref_self)
+            # exact real ties: which side wins is rounding noise (the
+            # reference's own PSA and Vose disagree on such rows), so every
+            # differing row must be a certified tie, and ties stay rare
+            assert diff.size <= max(16, w.size // 50), diff.size
             assert all(m < 1e-9 for m in near_tie_margins(w, ws.total, diff))
         else:
             assert diff.size == 0, ci
