@@ -225,12 +225,88 @@ __device__ __forceinline__ i64 rule_word(const RowT *tab, u64 word, i64 span, in
     return (frac * avg < (double)r.tw) ? (lo + k + 1) : (i64)r.alias;
 }
 
-// One CTA per section (grid-strided over [first, first+count)); the rows of
-// the section are copied into shared memory once, then every draw of the
-// section reads its row from there.  STAGE=false reads rows from global
-// memory (sections too large for shared memory).
+// Draw pair (d0, d1) of output slots (o0, o0 + 1) written with 16-byte
+// stores where possible.  `par` = 1 when o0 is not 16-byte aligned: then
+// lane t stores (d1 of t, d0 of t+1) as one vector and the warp's two end
+// elements with 8-byte stores.  v0/v1: whether each draw of the pair is in
+// range.  All lanes of the warp must call this (shuffles).
+__device__ __forceinline__ void store_pair(i64 *o0, i64 d0, i64 d1, bool v0, bool v1, int par,
+                                           int lane)
+{
+    if (par == 0) {
+        if (v0 && v1) {
+            *reinterpret_cast<longlong2 *>(o0) = make_longlong2(d0, d1);
+        } else {
+            if (v0) o0[0] = d0;
+            if (v1) o0[1] = d1;
+        }
+        return;
+    }
+    const i64 nx = __shfl_down_sync(0xffffffffu, d0, 1);
+    const bool nv = __shfl_down_sync(0xffffffffu, (int)v0, 1) != 0;
+    const bool vec = lane < 31 && v1 && nv;
+    const bool prev_vec = __shfl_up_sync(0xffffffffu, (int)vec, 1) != 0 && lane > 0;
+    if (vec) *reinterpret_cast<longlong2 *>(o0 + 1) = make_longlong2(d1, nx);
+    else if (v1) o0[1] = d1;
+    if (v0 && !prev_vec) o0[0] = d0;
+}
+
+// Fast-mode interior of a section (f32 rows staged in shared memory, span
+// 2^b): pairs q in [qa, qb) with qb - qa a multiple of the CTA size, every
+// draw in range.  Pair q is one Philox4x32-10 call (counter low word
+// cl0 + q, high word ch), its two 64-bit words are draws 2q and 2q + 1 of
+// ob.  Indices fit 32 bits (u32 aliases); outputs are written as int64 with
+// 16-byte stores (see store_pair for the misaligned case).
+__device__ __forceinline__ void fast_pairs_f32(const RowF32 *tab, u32 cl0, u32 ch, u64 strm,
+                                               const KeySched32 &ks, i64 *ob, u32 qa, u32 qb,
+                                               int b, u32 lo1, double avg, int par, int lane)
+{
+    const u32 sl = (u32)strm, sh = (u32)(strm >> 32);
+    const int sk = 32 - b;
+    const u64 fmask = (1ull << (53 - b)) - 1;
+    for (u32 q = qa + threadIdx.x; q < qb; q += blockDim.x) {
+        uint4 c = make_uint4(cl0 + q, ch, sl, sh);
+#pragma unroll
+        for (int r = 0; r < 10; ++r) {
+            const u32 hi0 = __umulhi(AK_PH4_M0, c.x), lo0 = AK_PH4_M0 * c.x;
+            const u32 hi1 = __umulhi(AK_PH4_M1, c.z), lo1_ = AK_PH4_M1 * c.z;
+            c = make_uint4(hi1 ^ c.y ^ ks.k[r].x, lo1_, hi0 ^ c.w ^ ks.k[r].y, lo0);
+        }
+        u32 d[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const u32 wl = h ? c.z : c.x, wh = h ? c.w : c.y;
+            const u64 word = ((u64)wh << 32) | wl;
+            const u32 k = wh >> sk;
+            const u64 f = (word >> 11) & fmask;
+            const double frac =
+                __longlong_as_double((long long)(0x3FF0000000000000ull | (f << (b - 1)))) - 1.0;
+            const uint2 row = *reinterpret_cast<const uint2 *>(tab + k);
+            d[h] = (frac * avg < (double)__uint_as_float(row.x)) ? lo1 + k : row.y;
+        }
+        i64 *p = ob + 2 * (u64)q;
+        if (par == 0) {
+            *reinterpret_cast<longlong2 *>(p) = make_longlong2((long long)d[0], (long long)d[1]);
+        } else {
+            const u32 nx = __shfl_down_sync(0xffffffffu, d[0], 1);
+            if (lane < 31) *reinterpret_cast<longlong2 *>(p + 1) = make_longlong2((long long)d[1], (long long)nx);
+            else p[1] = (i64)d[1];
+            if (lane == 0) p[0] = (i64)d[0];
+        }
+    }
+}
+
+// Sectioned sampling.  The draws of sections [first, first+count) form one
+// section-major index space (offsets = exclusive prefix of counts); CTA b
+// takes the contiguous slice [D*b/G, D*(b+1)/G) of it, so every CTA does the
+// same number of draws whatever the section sizes.  Walking its slice, a CTA
+// stages each section's rows in shared memory once (cp.async.bulk +
+// mbarrier) and serves every draw from there.  Each thread produces two
+// consecutive draws per step (one Philox4x32-10 call in the fast mode) and
+// the warp writes them as 16-byte stores.  STAGE=false reads rows from
+// global memory (sections too large for shared memory).
 template <typename RowT, int MODE, bool STAGE>
-__global__ void __launch_bounds__(1024) k_sample_sectioned(
+__global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
     const RowT *__restrict__ rows, u64 n, double avg, u64 S, const i64 *__restrict__ counts,
     const i64 *__restrict__ offsets, u64 first, u64 count, u64 seed, u64 stream_id, u64 ctr0,
     i64 *__restrict__ out, i64 out_base)
@@ -238,6 +314,7 @@ __global__ void __launch_bounds__(1024) k_sample_sectioned(
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) u64 bar;
     RowT *srows = reinterpret_cast<RowT *>(smem_raw);
+    const int lane = threadIdx.x & 31;
     u32 phase = 0;
     if (STAGE && threadIdx.x == 0) {
         mbar_init(&bar, 1);
@@ -246,17 +323,38 @@ __global__ void __launch_bounds__(1024) k_sample_sectioned(
     __syncthreads();
     const KeySched64 ks64 = sched64(seed);
     const KeySched32 ks32 = sched32(seed);
-    for (u64 sj = blockIdx.x; sj < count; sj += gridDim.x) {
-        const u64 j = first + sj;
+    // this CTA's slice of the pass's draw space
+    const u64 last = first + count - 1;
+    const i64 Dbeg = offsets[first];
+    const i64 Dend = offsets[last] + counts[last];
+    const u64 D = (u64)(Dend - Dbeg);
+    const i64 s0 = Dbeg + (i64)(((unsigned __int128)D * blockIdx.x) / gridDim.x);
+    const i64 s1 = Dbeg + (i64)(((unsigned __int128)D * (blockIdx.x + 1)) / gridDim.x);
+    if (s0 >= s1) return;
+    // the section holding draw s0: greatest j with offsets[j] <= s0
+    u64 a = first, b = last;
+    while (a < b) {
+        const u64 mid = (a + b + 1) >> 1;
+        if (offsets[mid] <= s0) a = mid;
+        else b = mid - 1;
+    }
+    for (u64 j = a; j <= last; ++j) {
+        const i64 oj = offsets[j];
+        if (oj >= s1) break;
         const i64 mj = counts[j];
         if (mj <= 0) continue;
+        // draws [ia, ib) of section j belong to this CTA
+        const i64 ia = s0 > oj ? s0 - oj : 0;
+        const i64 ib = s1 < oj + mj ? s1 - oj : mj;
+        if (ia >= ib) continue;
         const u64 lo = j * S;
         const u64 hi = lo + S < n ? lo + S : n;
         const i64 span = (i64)(hi - lo);
         const bool pow2 = span >= 2 && (span & (span - 1)) == 0;
-        const int b = pow2 ? __ffsll(span) - 1 : 0;
+        const int bb = pow2 ? __ffsll(span) - 1 : 0;
         const RowT *src = rows + lo;
         if (STAGE) {
+            __syncthreads();  // the previous section's rows are no longer read
             const u32 bytes = (u32)(span * sizeof(RowT));
             if ((((uintptr_t)src) & 15) == 0 && (bytes & 15) == 0) {
                 if (threadIdx.x == 0) {
@@ -272,35 +370,52 @@ __global__ void __launch_bounds__(1024) k_sample_sectioned(
         }
         const RowT *tab = STAGE ? srows : src;
         const u64 strm = ak_derive(seed, stream_id, j, AK_SALT_SECTION);
-        i64 *o = out + (offsets[j] - out_base);
-        const u64 um = (u64)mj;
-        if (MODE == AK_RNG_REFERENCE) {
-            constexpr int U = 2;
-            for (u64 bb = 0; bb < um; bb += (u64)blockDim.x * U) {
-                u64 wd[U];
-#pragma unroll
-                for (int t = 0; t < U; ++t)
-                    wd[t] = philox64_sched(ctr0 + bb + (u64)t * blockDim.x + threadIdx.x, strm, ks64);
-#pragma unroll
-                for (int t = 0; t < U; ++t) {
-                    const u64 i = bb + (u64)t * blockDim.x + threadIdx.x;
-                    if (i < um) o[i] = rule_word(tab, wd[t], span, b, pow2, (i64)lo, avg);
-                }
-            }
-        } else {
-            // counters ctr0+i, paired on even 64-bit counter values: thread t
-            // owns pair p -> draws i = 2p - (ctr0 & 1) and i + 1.
-            const u64 off = ctr0 & 1;
-            const u64 npairs = (um + off + 1) / 2;
-            for (u64 p = threadIdx.x; p < npairs; p += blockDim.x) {
+        i64 *o = out + (oj - out_base);
+        // pairs: pair p holds draws (2p - poff, 2p - poff + 1).  The fast RNG
+        // pairs draws on its call boundary (counter ctr0 + i even); the
+        // reference RNG pairs them on the 16-byte output boundary.
+        const int obit = (int)(((uintptr_t)o >> 3) & 1);
+        const i64 poff = MODE == AK_RNG_REFERENCE ? (i64)obit : (i64)(ctr0 & 1);
+        const int par = MODE == AK_RNG_REFERENCE ? 0 : (int)((obit + (int)poff) & 1);
+        const i64 p0 = (ia + poff) >> 1, p1 = (ib - 1 + poff) >> 1;  // inclusive
+        // checked pairs [ps, pe] (every lane of the CTA iterates together)
+        auto generic = [&](i64 ps, i64 pe) {
+            for (i64 pb = ps; pb <= pe; pb += blockDim.x) {
+                const i64 p = pb + threadIdx.x;
+                const i64 i0 = 2 * p - poff;
+                const bool v0 = p <= pe && i0 >= ia && i0 < ib;
+                const bool v1 = p <= pe && i0 + 1 >= ia && i0 + 1 < ib;
                 u64 w0, w1;
-                philox32_sched((ctr0 >> 1) + p, strm, ks32, w0, w1);
-                const i64 i0 = (i64)(2 * p) - (i64)off;
-                if (i0 >= 0 && (u64)i0 < um) o[i0] = rule_word(tab, w0, span, b, pow2, (i64)lo, avg);
-                if ((u64)(i0 + 1) < um) o[i0 + 1] = rule_word(tab, w1, span, b, pow2, (i64)lo, avg);
+                if (MODE == AK_RNG_REFERENCE) {
+                    w0 = philox64_sched(ctr0 + (u64)i0, strm, ks64);
+                    w1 = philox64_sched(ctr0 + (u64)i0 + 1, strm, ks64);
+                } else {
+                    philox32_sched(((ctr0 + (u64)i0) >> 1), strm, ks32, w0, w1);
+                }
+                const i64 d0 = rule_word(tab, w0, span, bb, pow2, (i64)lo, avg);
+                const i64 d1 = rule_word(tab, w1, span, bb, pow2, (i64)lo, avg);
+                store_pair(o + i0, d0, d1, v0, v1, par, lane);
+            }
+        };
+        if (MODE == AK_RNG_PHILOX4X32 && sizeof(RowT) == 8 && STAGE && pow2) {
+            // interior pairs q = p - p0 in [qa, qa + nfast): both draws in
+            // range, the call counter's high word constant, whole CTA steps
+            const i64 np = p1 - p0 + 1;
+            const i64 qa = (2 * p0 - poff >= ia) ? 0 : 1;
+            const i64 qb = np - ((2 * p1 - poff + 1 < ib) ? 0 : 1);
+            const u64 cb = (ctr0 >> 1) + (u64)p0;
+            i64 nfast = qb > qa ? ((qb - qa) / (i64)blockDim.x) * (i64)blockDim.x : 0;
+            if ((u64)(u32)cb + (u64)(qa + nfast) > 0xFFFFFFFFull) nfast = 0;
+            if (nfast > 0) {
+                if (qa > 0) generic(p0, p0 + qa - 1);
+                fast_pairs_f32(reinterpret_cast<const RowF32 *>(tab), (u32)cb, (u32)(cb >> 32),
+                               strm, ks32, o + (2 * p0 - poff), (u32)qa, (u32)(qa + nfast), bb,
+                               (u32)(lo + 1), avg, par, lane);
+                if (qa + nfast < np) generic(p0 + qa + nfast, p1);
+                continue;
             }
         }
-        if (STAGE) __syncthreads();  // rows buffer reused by the next section
+        generic(p0, p1);
     }
 }
 
@@ -338,7 +453,6 @@ int launch_sectioned_t(const void *rows, u64 n, double avg, u64 S, const i64 *co
     if (STAGE) AK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = STAGE ? (smem > 110 * 1024 ? 1 : 2) : 2;
     u64 g = (u64)ak_num_sms() * per_sm;
-    if (g > count) g = count;
     kern<<<(unsigned)g, 1024, smem, st>>>((const RowT *)rows, n, avg, S, counts, offsets, first,
                                           count, seed, sid, ctr0, out, out_base);
     AK_LAUNCH_CHECK("k_sample_sectioned");

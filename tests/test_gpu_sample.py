@@ -75,7 +75,7 @@ def test_random_tables_bit_exact(rng, dtype):
         tw, al = t.to_numpy()  # the device table as the reference would see it
         rt = O.Table(tw, al, n, tot)
         seed = int(rng.integers(2**63))
-        ctr = int(rng.integers(2**64)) if trial % 4 == 0 else int(rng.integers(1000))
+        ctr = int(rng.integers(2**64, dtype=np.uint64)) if trial % 4 == 0 else int(rng.integers(1000))
         got = ak.sample_batch(t, 50_000, ak.RngStream(seed, 3, ctr)).cpu().numpy()
         assert np.array_equal(got, O.sample_batch(rt, 50_000, seed, 3, ctr))
         for S in (1, 7, 64, 1000, 1 << 13, 1 << 14, 10**9):
@@ -160,3 +160,63 @@ def test_frequency_counts_device():
     with pytest.raises(ak.IndexOutOfRange):
         ak.frequency_counts(torch.tensor([0, 1], device=DEV), 3)
     assert ak.frequency_counts(torch.empty(0, dtype=torch.int64, device=DEV), 2).tolist() == [0, 0]
+
+
+def philox4x32_words(call: np.ndarray, strm: int, seed: int):
+    """numpy Philox4x32-10 (Random123 constants) of counters (call lo, call
+    hi, strm lo, strm hi) under key (seed lo, seed hi): the two 64-bit words
+    of every call (the GPU-native stream of rng="philox4x32")."""
+    M0, M1, W0, W1, m32 = 0xD2511F53, 0xCD9E8D57, 0x9E3779B9, 0xBB67AE85, 0xFFFFFFFF
+    call = call.astype(np.uint64)
+    c0 = call & np.uint64(m32)
+    c1 = call >> np.uint64(32)
+    c2 = np.full_like(c0, strm & m32)
+    c3 = np.full_like(c0, strm >> 32)
+    k0, k1 = seed & m32, seed >> 32
+    for _ in range(10):
+        p0 = c0 * np.uint64(M0)
+        p1 = c2 * np.uint64(M1)
+        hi0, lo0 = p0 >> np.uint64(32), p0 & np.uint64(m32)
+        hi1, lo1 = p1 >> np.uint64(32), p1 & np.uint64(m32)
+        c0, c1, c2, c3 = hi1 ^ c1 ^ np.uint64(k0), lo1, hi0 ^ c3 ^ np.uint64(k1), lo0
+        k0, k1 = (k0 + W0) & m32, (k1 + W1) & m32
+    return (c1 << np.uint64(32)) | c0, (c3 << np.uint64(32)) | c2
+
+
+def fast_section_reference(tw, al, avg, lo, span, seed, strm, ctr0, m):
+    v = np.uint64(ctr0) + np.arange(m, dtype=np.uint64)
+    a, b = philox4x32_words(v >> np.uint64(1), strm, seed)
+    word = np.where((v & np.uint64(1)) == 0, a, b)
+    u = (word >> np.uint64(11)).astype(np.float64) * 2.0**-53
+    return O.rule(tw, al, avg, u, lo, span)
+
+
+@pytest.mark.parametrize("ctr0", [0, 5, 2**32 - 3])
+def test_fast_rng_sectioned_bit_exact(ctr0):
+    """rng="philox4x32": the sectioned kernel (interior fast path, checked
+    edges, misaligned 16-byte stores, several passes per call) against a
+    numpy restatement of the GPU-native stream."""
+    g = np.random.default_rng(ctr0 + 1)
+    n, S, M = 3 * 4096 + 1000, 4096, 1_500_003
+    w = (g.random(n) + 1e-3).astype(np.float32)
+    ws = ak.make_weight_set(torch.from_numpy(w).to(DEV))
+    t = ak.psa_construct(ws)
+    tw, al = t.to_numpy()
+    seed, stream = 0x1234_5678_9ABC, 11
+    asg = ak.assign_sections(n, S, M, seed, stream)
+    want = np.concatenate([
+        fast_section_reference(tw, al, t.average, j * S, min((j + 1) * S, n) - j * S, seed,
+                               O.derive_stream(seed, stream, j, O.SALT_SECTION), ctr0,
+                               int(asg.counts[j]))
+        for j in range(asg.n_sections)])
+    got = ak.sectioned_sample(t, S, M, ak.RngStream(seed, stream, ctr0), rng="philox4x32")
+    assert np.array_equal(got.cpu().numpy(), want)
+    # pass-by-pass into a buffer offset by one element (odd 8-byte alignment)
+    from paper_2106_12270_b200.sample import sectioned_sample_into
+    counts = torch.from_numpy(asg.counts).to(DEV)
+    offs = torch.from_numpy(np.concatenate([[0], np.cumsum(asg.counts)[:-1]])).to(DEV)
+    buf = torch.full((M + 1,), -1, dtype=torch.int64, device=DEV)
+    for first, count in ((0, 1), (1, 2), (3, asg.n_sections - 3)):
+        sectioned_sample_into(t, S, counts, offs, first, count, ak.RngStream(seed, stream, ctr0),
+                              buf[1:], 0, "philox4x32")
+    assert np.array_equal(buf[1:].cpu().numpy(), want)
