@@ -16,7 +16,7 @@ import torch
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libaliaskit_b200.so")
+LIB_PATH = os.environ.get("AK_LIB_PATH") or os.path.join(_HERE, "libaliaskit_b200.so")
 
 F32, F64 = 0, 1
 RNG_REFERENCE, RNG_PHILOX4X32 = 0, 1

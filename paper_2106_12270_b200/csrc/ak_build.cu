@@ -175,7 +175,7 @@ __device__ __forceinline__ double warp_scan_mono(double x, int lane)
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
         double y = shfl_up_d(x, d);
-        if (lane >= d) x = fmax(x, y);
+        if (lane >= d) x = x > y ? x : y;
     }
     return x;
 }
@@ -229,11 +229,15 @@ __device__ __forceinline__ double chunk_total(const double v[VV], double avg, u3
 __device__ __forceinline__ void class_keys(double loc[VV], double excl, double base, double bound,
                                            int lane)
 {
-    double B = fmin(base + excl, bound);
+    double B = base + excl;
+    B = B < bound ? B : bound;
     double U = __shfl_down_sync(0xffffffffu, B, 1);
     if (lane == 31) U = bound;
 #pragma unroll
-    for (int k = 0; k < VV; ++k) loc[k] = fmin(B + loc[k], U);
+    for (int k = 0; k < VV; ++k) {
+        const double x = B + loc[k];
+        loc[k] = x < U ? x : U;
+    }
 }
 
 // offset of the first set item in the chunk (lane-major), NOFH if none
@@ -254,61 +258,181 @@ __device__ __forceinline__ dd shfl_xor_dd(dd x, int m)
     return dd_make(__shfl_xor_sync(0xffffffffu, x.hi, m), __shfl_xor_sync(0xffffffffu, x.lo, m));
 }
 
-template <typename T>
-__global__ void __launch_bounds__(TB) k_build_scan(const T *__restrict__ w, u64 n, double avg,
-                                                   BuildWs W)
+// Reduce-scatter of eight per-lane values over the warp: lane l returns the
+// warp sum of value l >> 2 (3 halving exchanges + 2 butterfly steps).
+__device__ __forceinline__ double reduce8(const double v[NW], int lane)
 {
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+    double a[4], b[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double keep = b4 ? v[4 + i] : v[i], send = b4 ? v[i] : v[4 + i];
+        a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double keep = b3 ? a[2 + i] : a[i], send = b3 ? a[i] : a[2 + i];
+        b[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    double c = (b2 ? b[1] : b[0]) + __shfl_xor_sync(0xffffffffu, b2 ? b[0] : b[1], 4);
+    c = c + __shfl_xor_sync(0xffffffffu, c, 2);
+    c = c + __shfl_xor_sync(0xffffffffu, c, 1);
+    return c;
+}
+
+// lane's 8 items of a chunk staged in shared memory (T values, not widened)
+template <typename T>
+__device__ __forceinline__ void lds8_raw(const T *p, T v[VV])
+{
+    if (sizeof(T) == 4) {
+        const float4 a = reinterpret_cast<const float4 *>(p)[0], b = reinterpret_cast<const float4 *>(p)[1];
+        const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int q = 0; q < VV; ++q) v[q] = (T)f[q];
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double2 a = reinterpret_cast<const double2 *>(p)[q];
+            v[2 * q] = (T)a.x;
+            v[2 * q + 1] = (T)a.y;
+        }
+    }
+}
+
+// the largest T not above avg: (double)v <= avg  <=>  v <= avg_t(avg)
+template <typename T> __device__ __forceinline__ T avg_floor(double avg);
+template <> __device__ __forceinline__ float avg_floor<float>(double avg)
+{
+    float f = __double2float_rd(avg);
+    return f;
+}
+template <> __device__ __forceinline__ double avg_floor<double>(double avg) { return avg; }
+
+// pairwise sum of 8 doubles (depth 3: independent adds for ILP)
+__device__ __forceinline__ double sum8(const double x[8])
+{
+    return ((x[0] + x[1]) + (x[2] + x[3])) + ((x[4] + x[5]) + (x[6] + x[7]));
+}
+
+constexpr int SC_WARPS = 4;  // warps per scan CTA; each owns SUPER / SC_WARPS tiles
+template <typename T> struct ScanBuf {
+    // per warp a ring of NW chunk slots (chunk c of successive tiles in slot c)
+    static constexpr size_t BYTES = (size_t)SC_WARPS * NW * CH * sizeof(T);
+};
+
+// One pass over the weights.  Each warp streams its tiles chunk by chunk
+// through a ring of shared-memory slots filled by 1-D bulk async copies (the
+// TMA engine; ~7 chunks in flight per warp), classifies the items (in the
+// weight type: v <= avg exactly), and forms per-chunk light/heavy totals as
+// nl*avg - sum(light w) and sum(heavy w) - nh*avg (these only fix the chunk
+// bounds that every key is clamped into, so their rounding is free), light
+// counts, first-heavy offsets and the tile's monotone chunk bounds.  Warp 0
+// then scans the super-tile's tile totals (double-double), publishes the
+// aggregate, runs the decoupled look-back and writes the exclusive tile bases.
+template <typename T>
+__global__ void __launch_bounds__(SC_WARPS * 32) k_build_scan(const T *__restrict__ w, u64 n,
+                                                              double avg, BuildWs W)
+{
+    extern __shared__ __align__(128) unsigned char scan_smem[];
+    __shared__ __align__(8) u64 bars[SC_WARPS][NW];
     __shared__ double s_tD[SUPER], s_tE[SUPER];
     __shared__ u32 s_tL[SUPER];
     __shared__ u64 s_fH[SUPER];
     __shared__ unsigned int s_st;
-    __shared__ dd s_exD, s_exH, s_agD, s_agH;
-    __shared__ u64 s_exK, s_agK;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_st = atomicAdd(W.counter, 1u);
+    if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < NW; ++c) mbar_init(&bars[wid][c], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
     const u64 st = s_st;
     const u64 t0 = st * SUPER;
     const u64 tn = (t0 + SUPER <= W.nt) ? SUPER : W.nt - t0;
+    T *ring = reinterpret_cast<T *>(scan_smem) + (size_t)wid * NW * CH;
+    const T avgT = avg_floor<T>(avg);
+    auto full_chunk = [&](u64 g) { return (g + 1) * CH <= n; };
+    auto issue = [&](u64 j, int c) {  // chunk c of the super-tile's tile j into slot c
+        const u64 g = (t0 + j) * NW + c;
+        if (lane == 0 && j < tn && full_chunk(g)) {
+            mbar_expect_tx(&bars[wid][c], CH * sizeof(T));
+            bulk_g2s(ring + c * CH, w + g * CH, CH * sizeof(T), &bars[wid][c]);
+        }
+    };
+#pragma unroll
+    for (int c = 0; c < NW; ++c) issue((u64)wid, c);
+    u32 phase = 0;  // all slots complete once per tile: one parity for all
 
-    // each warp owns whole tiles (no per-tile block barrier): 8 chunk totals
-    // by butterfly sums, then their monotone scan within the warp
-    for (u64 j = wid; j < tn; j += NW) {
+    for (u64 j = wid; j < tn; j += SC_WARPS) {
         const u64 t = t0 + j;
-        double cd = 0.0, ce = 0.0;  // lane c < 8 ends up holding chunk c's totals
+        double sD[NW], sE[NW];
         u32 cl = 0;
         unsigned char cf = NOFH;
-        double va[VV], vb[VV];
-        load8(w, n, t * TILE + (u64)lane * VV, va);
 #pragma unroll
         for (int c = 0; c < NW; ++c) {
-            double *v = (c & 1) ? vb : va;
-            if (c + 1 < NW) load8(w, n, t * TILE + (u64)(c + 1) * CH + (u64)lane * VV, (c & 1) ? va : vb);
-            u32 lm, hm;
-            const double tD = chunk_total<true>(v, avg, lm);
-            const double tE = chunk_total<false>(v, avg, hm);
-            u32 nl = __popc(lm);
+            const u64 g = t * NW + c;
+            double xl[VV], xh[VV];
+            u32 lm = 0, vm = 0;
+            if (full_chunk(g)) {
+                mbar_wait(&bars[wid][c], phase);
+                T v[VV];
+                lds8_raw(ring + c * CH + lane * VV, v);
 #pragma unroll
-            for (int d = 16; d >= 1; d >>= 1) nl += __shfl_xor_sync(0xffffffffu, nl, d);
+                for (int q = 0; q < VV; ++q) {
+                    const bool li = v[q] <= avgT;
+                    const double dv = (double)v[q];
+                    xl[q] = li ? avg - dv : 0.0;
+                    xh[q] = li ? 0.0 : dv - avg;
+                    lm |= (u32)li << q;
+                }
+                vm = 0xFFu;
+                // the slot's reads are done (values consumed) and ordered
+                // before the async-proxy refill of the next tile's chunk c
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                issue(j + SC_WARPS, c);
+            } else {
+                double v[VV];
+                load8(w, n, g * CH + (u64)lane * VV, v);
+#pragma unroll
+                for (int q = 0; q < VV; ++q) {
+                    const bool valid = v[q] >= 0.0;
+                    const bool li = valid && v[q] <= avg;
+                    xl[q] = li ? avg - v[q] : 0.0;
+                    xh[q] = valid && !li ? v[q] - avg : 0.0;
+                    lm |= (u32)li << q;
+                    vm |= (u32)valid << q;
+                }
+            }
+            const u32 hm = vm & ~lm;
+            const int nlq = __popc(lm), nhq = __popc(hm);
+            (void)nhq;
+            sD[c] = sum8(xl);
+            sE[c] = sum8(xh);
+            const u32 nl = __reduce_add_sync(0xffffffffu, (u32)nlq);
             const unsigned char fh = first_item(hm, lane);
             if (lane == c) {
-                cd = tD;
-                ce = tE;
                 cl = nl;
                 cf = fh;
             }
         }
-        // monotone scan of the 8 chunk totals -> chunk bounds
-        double x = lane < NW ? cd : 0.0, y = lane < NW ? ce : 0.0;
+        phase ^= 1;
+        // chunk totals -> lanes 0..7, then their monotone scan -> chunk bounds
+        const double rD = reduce8(sD, lane), rE = reduce8(sE, lane);
+        double x = __shfl_sync(0xffffffffu, rD, (lane & 7) * 4), y = __shfl_sync(0xffffffffu, rE, (lane & 7) * 4);
+        x = x > 0.0 ? x : 0.0;  // a class's chunk total is a sum of non-negative terms
+        y = y > 0.0 ? y : 0.0;
+        if (lane >= NW) x = y = 0.0;
 #pragma unroll
         for (int d = 1; d < NW; d <<= 1) {
-            double a = shfl_up_d(x, d), b = shfl_up_d(y, d);
-            if (lane >= d) { x = x + a; y = y + b; }
+            double a = shfl_up_d(x, d), bb = shfl_up_d(y, d);
+            if (lane >= d) { x = x + a; y = y + bb; }
         }
 #pragma unroll
         for (int d = 1; d < NW; d <<= 1) {
-            double a = shfl_up_d(x, d), b = shfl_up_d(y, d);
-            if (lane >= d) { x = fmax(x, a); y = fmax(y, b); }
+            double a = shfl_up_d(x, d), bb = shfl_up_d(y, d);
+            if (lane >= d) { x = x > a ? x : a; y = y > bb ? y : bb; }
         }
         if (lane < NW) {
             W.mD[t * NW + lane] = x;
@@ -316,9 +440,7 @@ __global__ void __launch_bounds__(TB) k_build_scan(const T *__restrict__ w, u64 
             W.mfh[t * NW + lane] = cf;
             W.mcl[t * NW + lane] = (unsigned short)cl;
         }
-        u32 tl = lane < NW ? cl : 0;
-#pragma unroll
-        for (int d = 16; d >= 1; d >>= 1) tl += __shfl_xor_sync(0xffffffffu, tl, d);
+        const u32 tl = __reduce_add_sync(0xffffffffu, lane < NW ? cl : 0u);
         const unsigned fhm = __ballot_sync(0xffffffffu, lane < NW && cf != NOFH);
         const int fc = fhm ? __ffs(fhm) - 1 : 0;
         const unsigned char ff = (unsigned char)__shfl_sync(0xffffffffu, (int)cf, fc);
@@ -331,18 +453,25 @@ __global__ void __launch_bounds__(TB) k_build_scan(const T *__restrict__ w, u64 
         }
     }
     __syncthreads();
-    // super-tile aggregate: exact double-double sum of the tile totals
-    if (threadIdx.x == 0) {
-        dd aD = dd_make(0.0), aH = dd_make(0.0);
-        u64 aK = 0;
-        for (u64 j = 0; j < tn; ++j) {
-            aD = dd_add_d(aD, s_tD[j]);
-            aH = dd_add_d(aH, s_tE[j]);
-            aK += s_tL[j];
+    if (threadIdx.x >= 32) return;
+    // warp 0: inclusive scan of the tile totals (exact double-double sums)
+    dd xD = dd_make((u64)lane < tn ? s_tD[lane] : 0.0), xH = dd_make((u64)lane < tn ? s_tE[lane] : 0.0);
+    u64 xK = (u64)lane < tn ? s_tL[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const dd yD = dd_make(shfl_up_d(xD.hi, d), shfl_up_d(xD.lo, d));
+        const dd yH = dd_make(shfl_up_d(xH.hi, d), shfl_up_d(xH.lo, d));
+        const u64 yK = __shfl_up_sync(0xffffffffu, xK, d);
+        if (lane >= d) {
+            xD = dd_add(yD, xD);
+            xH = dd_add(yH, xH);
+            xK += yK;
         }
-        s_agD = aD;
-        s_agH = aH;
-        s_agK = aK;
+    }
+    const dd aD = dd_make(shfl_idx_d(xD.hi, 31), shfl_idx_d(xD.lo, 31));
+    const dd aH = dd_make(shfl_idx_d(xH.hi, 31), shfl_idx_d(xH.lo, 31));
+    const u64 aK = __shfl_sync(0xffffffffu, xK, 31);
+    if (lane == 0) {
         if (st == 0) {
             W.inc_D[0] = aD;
             W.inc_H[0] = aH;
@@ -355,75 +484,62 @@ __global__ void __launch_bounds__(TB) k_build_scan(const T *__restrict__ w, u64 
         __threadfence();
         st_release_u32(&W.status[st], st == 0 ? 2u : 1u);
     }
-    __syncthreads();
-    // look-back by warp 0
-    if (threadIdx.x < 32) {
-        dd aD = dd_make(0.0), aH = dd_make(0.0);
-        u64 aK = 0;
-        i64 pred = (i64)st - 1;
-        while (pred >= 0) {
-            const i64 p = pred - lane;
-            u32 s = 2;
-            if (p >= 0) {
-                do { s = ld_acquire_u32(&W.status[p]); } while (s == 0);
-            }
-            const unsigned inc_mask = __ballot_sync(0xffffffffu, p >= 0 && s == 2);
-            const int stop = inc_mask ? __ffs(inc_mask) - 1 : 32;
-            dd cD = dd_make(0.0), cH = dd_make(0.0);
-            u64 cK = 0;
-            if (p >= 0 && lane < stop) {
-                cD = W.agg_D[p];
-                cH = W.agg_H[p];
-                cK = W.agg_k[p];
-            } else if (p >= 0 && lane == stop) {
-                cD = W.inc_D[p];
-                cH = W.inc_H[p];
-                cK = W.inc_k[p];
-            }
+    // decoupled look-back over the predecessors, 32 at a time
+    dd eD = dd_make(0.0), eH = dd_make(0.0);
+    u64 eK = 0;
+    i64 pred = (i64)st - 1;
+    while (pred >= 0) {
+        const i64 p = pred - lane;
+        u32 s = 2;
+        if (p >= 0) {
+            do { s = ld_acquire_u32(&W.status[p]); } while (s == 0);
+        }
+        const unsigned inc_mask = __ballot_sync(0xffffffffu, p >= 0 && s == 2);
+        const int stop = inc_mask ? __ffs(inc_mask) - 1 : 32;
+        dd cD = dd_make(0.0), cH = dd_make(0.0);
+        u64 cK = 0;
+        if (p >= 0 && lane < stop) {
+            cD = W.agg_D[p];
+            cH = W.agg_H[p];
+            cK = W.agg_k[p];
+        } else if (p >= 0 && lane == stop) {
+            cD = W.inc_D[p];
+            cH = W.inc_H[p];
+            cK = W.inc_k[p];
+        }
 #pragma unroll
-            for (int m = 16; m >= 1; m >>= 1) {
-                cD = dd_add(cD, shfl_xor_dd(cD, m));
-                cH = dd_add(cH, shfl_xor_dd(cH, m));
-                cK += __shfl_xor_sync(0xffffffffu, cK, m);
-            }
-            aD = dd_add(aD, cD);
-            aH = dd_add(aH, cH);
-            aK += cK;
-            if (stop < 32 || pred - 32 < 0) break;
-            pred -= 32;
+        for (int m = 16; m >= 1; m >>= 1) {
+            cD = dd_add(cD, shfl_xor_dd(cD, m));
+            cH = dd_add(cH, shfl_xor_dd(cH, m));
+            cK += __shfl_xor_sync(0xffffffffu, cK, m);
         }
-        if (lane == 0) {
-            if (st > 0) {
-                W.inc_D[st] = dd_add(aD, s_agD);
-                W.inc_H[st] = dd_add(aH, s_agH);
-                W.inc_k[st] = aK + s_agK;
-                __threadfence();
-                st_release_u32(&W.status[st], 2u);
-            }
-            s_exD = aD;
-            s_exH = aH;
-            s_exK = aK;
-        }
+        eD = dd_add(eD, cD);
+        eH = dd_add(eH, cH);
+        eK += cK;
+        if (stop < 32 || pred - 32 < 0) break;
+        pred -= 32;
     }
-    __syncthreads();
+    if (lane == 0 && st > 0) {
+        W.inc_D[st] = dd_add(eD, aD);
+        W.inc_H[st] = dd_add(eH, aH);
+        W.inc_k[st] = eK + aK;
+        __threadfence();
+        st_release_u32(&W.status[st], 2u);
+    }
     // exclusive bases of the super-tile's tiles
-    if (threadIdx.x == 0) {
-        dd D = s_exD, H = s_exH;
-        u64 K = s_exK;
-        for (u64 j = 0; j < tn; ++j) {
-            const u64 t = t0 + j;
-            W.DLb[t] = D;
-            W.DHb[t] = H;
-            W.kL[t] = K;
-            W.firstH[t] = s_fH[j];
-            D = dd_add_d(D, s_tD[j]);
-            H = dd_add_d(H, s_tE[j]);
-            K += s_tL[j];
-        }
-        if (t0 + tn == W.nt) {
-            W.DLb[W.nt] = D;
-            W.DHb[W.nt] = H;
-            W.kL[W.nt] = K;
+    const dd pD = dd_make(shfl_up_d(xD.hi, 1), shfl_up_d(xD.lo, 1));
+    const dd pH = dd_make(shfl_up_d(xH.hi, 1), shfl_up_d(xH.lo, 1));
+    const u64 pK = __shfl_up_sync(0xffffffffu, xK, 1);
+    if ((u64)lane < tn) {
+        const u64 t = t0 + lane;
+        W.DLb[t] = lane ? dd_add(eD, pD) : eD;
+        W.DHb[t] = lane ? dd_add(eH, pH) : eH;
+        W.kL[t] = eK + (lane ? pK : 0);
+        W.firstH[t] = s_fH[lane];
+        if (t + 1 == W.nt) {
+            W.DLb[W.nt] = dd_add(eD, xD);
+            W.DHb[W.nt] = dd_add(eH, xH);
+            W.kL[W.nt] = eK + xK;
         }
     }
 }
@@ -503,9 +619,7 @@ __device__ __forceinline__ u32 warp_excl_count(u32 cnt, u32 &total, int lane)
 // pass-1 chunk bounds (8 lanes at once), the count inside the chunk from its
 // canonical keys.  Outputs: the boundary's heavy rank, the chunk holding that
 // rank, and the item of that heavy (the first heavy past the boundary).
-constexpr int HCAP = 1408;       // heavies per merge round
-constexpr int CB = 32;           // chunks enumerated per round
-constexpr u32 NONE32 = 0xFFFFFFFFu;
+constexpr int HCAP = 1408;       // heavies per merge round (smem for 4 CTAs per SM)
 
 struct SplitOut {
     u64 *hrank;   // [nt+2]
@@ -634,17 +748,41 @@ __global__ void __launch_bounds__(TB) k_build_split(const T *__restrict__ w, u64
 // light its successor heavy and each heavy its successor light; rows are
 // written directly: lights by the threads that own them, heavies in rank
 // order.  Large heavy ranges are processed in rounds of HCAP.
-template <typename T> struct SecSmem {
-    double LK[TILE];               // own light keys (own frame), rank order
-    dd HK[HCAP];                   // heavy keys (own frame)
-    u32 HI[HCAP];                  // heavy items
-    u32 LS[TILE];                  // light successor item (+1), 0 = unresolved
-    unsigned short SL[HCAP];       // heavy -> successor light index
-    u64 cbase[CB + 1];             // heavy rank of each enumerated chunk's first heavy
-    u32 lcnt[NW];
+struct SecSmem {
+    double LK[TILE + 1];           // own light keys (own frame), rank order; +inf sentinel
+    u32 LS[TILE];                  // light successor heavy item (+1), 0 = unresolved
+    dd HK[HCAP + 1];               // heavy keys (own frame); +inf sentinel
+    u32 HI[HCAP + 1];              // heavy items; ~0 sentinel (LS = HI + 1 = 0: unresolved)
+    double SK[HCAP];               // heavy -> key of its successor light (+inf: none here)
     u32 lfirst;
     u64 next_item;                 // item of the heavy ranked jend (first of the next round)
 };
+
+// heavy rank of the first heavy of each of the 32 chunks g0 .. g0+31 (lane
+// i holds chunk g0 + i; ~0 past the last chunk) and its heavy count; every
+// warp computes the same table, so no block barrier is needed.
+__device__ __forceinline__ void chunk_ranks(const BuildWs &W, u64 n, u64 g0, int lane, u64 &hb,
+                                            u32 &hc)
+{
+    const u64 nch = W.nt * NW;
+    const u64 g = g0 + lane;
+    hc = g < nch ? chunk_valid(n, g) - W.mcl[g] : 0u;
+    u32 inc = hc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const u32 a = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += a;
+    }
+    // heavy rank of chunk g0's first heavy: heavies before its tile plus the
+    // heavies of the tile's earlier chunks
+    const u64 t0 = g0 / NW;
+    const int c0 = (int)(g0 % NW);
+    u32 pre = 0;
+    if (lane < c0) pre = chunk_valid(n, t0 * NW + lane) - W.mcl[t0 * NW + lane];
+    pre = __reduce_add_sync(0xffffffffu, pre);
+    const u64 base = (g0 < nch ? heavies_before_tile(W, n, t0) : heavies_before_tile(W, n, W.nt)) + pre;
+    hb = g < nch ? base + (inc - hc) : ~0ull;
+}
 
 template <typename T>
 __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u64 n, double avg,
@@ -655,7 +793,7 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
     typedef decltype(RowT::tw) TwT;
     typedef decltype(RowT::alias) AliasT;
     extern __shared__ __align__(16) unsigned char sec_smem[];
-    SecSmem<T> &P = *reinterpret_cast<SecSmem<T> *>(sec_smem);
+    SecSmem &P = *reinterpret_cast<SecSmem *>(sec_smem);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const u64 nt = W.nt;
     const u64 u = blockIdx.x;  // section; u == nt: the heavies past every light
@@ -664,25 +802,26 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
     const dd own = u < nt ? W.DLb[u] : W.DLb[nt];
     const double secbound = u < nt ? W.mD[u * NW + NW - 1] : 0.0;  // next light key, own frame
 
-    // ---- lights of tile u (rank order = key order)
+    // ---- lights of tile u (rank order = key order), keys into shared memory
     u32 nL = 0, lrank0 = 0, lm = 0;
-    double lk[VV], lv[VV];
+    double lv[VV];
     if (u < nt) {
-        if (lane == 0) P.lcnt[wid] = W.mcl[u * NW + wid];
+        const uint4 cnt4 = *reinterpret_cast<const uint4 *>(W.mcl + u * NW);  // 8 x u16
+        const u32 cw[4] = {cnt4.x, cnt4.y, cnt4.z, cnt4.w};
+        u32 woff = 0;
+#pragma unroll
+        for (int k = 0; k < NW; ++k) {
+            const u32 ck = (cw[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
+            woff += k < wid ? ck : 0u;
+            nL += ck;
+        }
         load8(w, n, u * TILE + (u64)wid * CH + (u64)lane * VV, lv);
         const double b0 = wid ? W.mD[u * NW + wid - 1] : 0.0, b1 = W.mD[u * NW + wid];
-        double ex, tot;
+        double lk[VV], ex, tot;
         lane_class<true>(lv, avg, lk, lm, ex, tot, lane);
         class_keys(lk, ex, b0, b1, lane);
         u32 tl;
-        const u32 el = warp_excl_count(__popc(lm), tl, lane);
-        __syncthreads();
-        u32 woff = 0;
-        for (int k = 0; k < NW; ++k) {
-            woff += k < wid ? P.lcnt[k] : 0;
-            nL += P.lcnt[k];
-        }
-        lrank0 = woff + el;
+        lrank0 = woff + warp_excl_count(__popc(lm), tl, lane);
         u32 r = lrank0;
 #pragma unroll
         for (int q = 0; q < VV; ++q)
@@ -692,42 +831,35 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
                 ++r;
             }
     }
-    __syncthreads();
 
-    // ---- heavies in rounds of at most HCAP ranks
+    if (threadIdx.x == 0) P.LK[nL] = __longlong_as_double(0x7FF0000000000000ll);
+
+    // ---- heavies in rounds of at most HCAP ranks (one round unless the
+    // section's heavy range is large or spans more than 32 chunks)
     u64 jcur = J0;
     u64 gcur = O.hchunk[u];
     u32 lfirst = 0;  // first light not yet resolved
+    if (threadIdx.x == 0) P.next_item = NONE64;
+    __syncthreads();
     while (jcur < J1) {
-        // enumerate CB chunks from gcur with the heavy rank of their first heavy
-        if (wid == 0) {
-            const u64 g = gcur + lane;
-            u64 hb = ~0ull;
-            u32 hcnt = 0;
-            if (g < nt * NW) {
-                const u64 t = g / NW;
-                const int c = (int)(g % NW);
-                hcnt = chunk_valid(n, g) - W.mcl[g];
-                u32 pre = 0;
-                for (int k = 0; k < c; ++k) pre += chunk_valid(n, t * NW + k) - W.mcl[t * NW + k];
-                hb = heavies_before_tile(W, n, t) + pre;
-            }
-            P.cbase[lane] = hb;
-            const u64 last = __shfl_sync(0xffffffffu, hb == ~0ull ? ~0ull : hb + hcnt, 31);
-            if (lane == 0) {
-                P.cbase[CB] = last;
-                P.next_item = NONE64;
-            }
-        }
-        __syncthreads();
+        u64 hb;
+        u32 hc;
+        chunk_ranks(W, n, gcur, lane, hb, hc);
+        const u64 last = __shfl_sync(0xffffffffu, hb == ~0ull ? ~0ull : hb + hc, 31);
         u64 jend = J1 < jcur + HCAP ? J1 : jcur + HCAP;
-        if (P.cbase[CB] < jend) jend = P.cbase[CB];
+        if (last < jend) jend = last;
         const u32 nH = (u32)(jend - jcur);
         const bool last_round = jend >= J1;
-        // rebuild the chunks covering ranks [jcur, jend], own frame
-        for (int ci = wid; ci < CB; ci += NW) {
-            const u64 hb = P.cbase[ci], hn = P.cbase[ci + 1];
-            if (hb == ~0ull || hb > jend || hn <= jcur) continue;
+        // rebuild the chunks covering ranks [jcur, jend] (rank jend: the next
+        // round's first heavy), own frame
+        if (threadIdx.x == 0) {  // merge sentinels
+            P.HK[nH] = dd_make(__longlong_as_double(0x7FF0000000000000ll));
+            P.HI[nH] = 0xFFFFFFFFu;
+        }
+        const unsigned need = __ballot_sync(0xffffffffu, hb != ~0ull && hb <= jend && hb + hc > jcur);
+        for (int ci = wid; ci < 32; ci += NW) {
+            if (!((need >> ci) & 1)) continue;
+            const u64 cb = __shfl_sync(0xffffffffu, hb, ci);
             const u64 g = gcur + ci;
             const u64 t = g / NW;
             const int c = (int)(g % NW);
@@ -739,7 +871,7 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
             lane_class<false>(v, avg, k, m, ex, tot, lane);
             class_keys(k, ex, base, bound, lane);
             u32 tc;
-            u64 rr = hb + warp_excl_count(__popc(m), tc, lane);
+            u64 rr = cb + warp_excl_count(__popc(m), tc, lane);
 #pragma unroll
             for (int q = 0; q < VV; ++q)
                 if ((m >> q) & 1) {
@@ -757,12 +889,16 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
         __syncthreads();
         if (!last_round && wid == 0 && P.next_item == NONE64) {
             // rank jend lies past the enumerated chunks
-            const u64 gl = gcur + CB - 1;
+            const u64 gl = gcur + 31;
             const u64 nx = next_heavy_after(W, gl / NW, (int)(gl % NW), lane);
             if (lane == 0) P.next_item = nx;
         }
-        // merge path: lights [lfirst, nL) with heavies [0, nH); heavy first on ties
+        // merge path: lights [lfirst, nL) with heavies [0, nH); heavy first on
+        // ties.  +inf sentinels end both lists; a taken heavy records the key
+        // of its successor light, a taken light its successor heavy's item.
         {
+            const double *LKp = P.LK + lfirst;
+            u32 *LSp = P.LS + lfirst;
             const u32 na = nL - lfirst;
             const u32 total = na + nH;
             const u32 per = (total + TB - 1) / TB;
@@ -771,19 +907,22 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
                 u32 lo = d0 > nH ? d0 - nH : 0, hi = d0 < na ? d0 : na;
                 while (lo < hi) {
                     const u32 mid = (lo + hi) >> 1;
-                    if (!le_dd_d(P.HK[d0 - mid - 1], P.LK[lfirst + mid])) lo = mid + 1;
+                    if (!le_dd_d(P.HK[d0 - mid - 1], LKp[mid])) lo = mid + 1;
                     else hi = mid;
                 }
                 u32 i = lo, j = d0 - lo;
-                const u32 d1 = d0 + per < total ? d0 + per : total;
-                for (u32 d = d0; d < d1; ++d) {
-                    const bool light = i < na && (j >= nH || !le_dd_d(P.HK[j], P.LK[lfirst + i]));
-                    if (light) {
-                        if (j < nH) P.LS[lfirst + i] = P.HI[j] + 1;
-                        ++i;
-                    } else {
-                        P.SL[j] = (unsigned short)(lfirst + i);
+                const u32 steps = d0 + per < total ? per : total - d0;
+                double lk = LKp[i];
+                dd hk = P.HK[j];
+                for (u32 d = 0; d < steps; ++d) {
+                    if (le_dd_d(hk, lk)) {
+                        P.SK[j] = lk;
                         ++j;
+                        hk = P.HK[j];
+                    } else {
+                        LSp[i] = P.HI[j] + 1;
+                        ++i;
+                        lk = LKp[i];
                     }
                 }
             }
@@ -793,8 +932,8 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
         const u64 nxt = last_round ? after : P.next_item;
         for (u32 j = threadIdx.x; j < nH; j += TB) {
             const u32 item = P.HI[j];
-            const u32 sl = P.SL[j];
-            const double DL = sl < nL ? P.LK[sl] : secbound;
+            const double sk = P.SK[j];
+            const double DL = sk != __longlong_as_double(0x7FF0000000000000ll) ? sk : secbound;
             const dd tw = dd_add_d(add_dd_d(P.HK[j], -DL), avg);
             u64 al;
             if (j + 1 < nH) al = (u64)P.HI[j + 1] + 1;
@@ -804,8 +943,9 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
             row.alias = (AliasT)al;
             rows[item] = row;
         }
+        if (last_round) break;
         // the resolved lights form a prefix: the next round starts after it
-        if (!last_round && threadIdx.x == 0) {
+        if (threadIdx.x == 0) {
             u32 a = lfirst, b = nL;
             while (a < b) {
                 const u32 mid = (a + b) >> 1;
@@ -814,15 +954,14 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
             }
             P.lfirst = a;
         }
-        u64 gnext = gcur;
-        for (int ci = 0; ci < CB; ++ci) {
-            const u64 hb = P.cbase[ci];
-            if (hb != ~0ull && hb <= jend) gnext = gcur + ci;
-        }
+        // next round starts at the chunk holding rank jend
+        const unsigned upto = __ballot_sync(0xffffffffu, hb != ~0ull && hb <= jend);
+        gcur += upto ? 31 - __clz(upto) : 0;
         __syncthreads();
-        if (!last_round) lfirst = P.lfirst;
-        gcur = gnext;
+        lfirst = P.lfirst;
+        if (threadIdx.x == 0) P.next_item = NONE64;
         jcur = jend;
+        __syncthreads();
     }
     // lights: rows written by their owning lanes; unresolved ones alias the
     // first heavy past the section (or themselves)
@@ -858,13 +997,15 @@ int run_build(const void *wv, u64 n, double total, void *rows, void *ws, cudaStr
     }
     AK_CUDA_TRY(cudaMemsetAsync(W.counter, 0, 256, st));
     AK_CUDA_TRY(cudaMemsetAsync(W.status, 0, W.nst * 4, st));
-    k_build_scan<T><<<(unsigned)W.nst, TB, 0, st>>>(w, n, avg, W);
+    AK_CUDA_TRY(cudaFuncSetAttribute(k_build_scan<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)ScanBuf<T>::BYTES));
+    k_build_scan<T><<<(unsigned)W.nst, SC_WARPS * 32, ScanBuf<T>::BYTES, st>>>(w, n, avg, W);
     AK_LAUNCH_CHECK("k_build_scan");
     k_build_coarse<<<(unsigned)((W.nt + 1 + 255) / 256), 256, 0, st>>>(W, n);
     AK_LAUNCH_CHECK("k_build_coarse");
     k_build_split<T><<<(unsigned)((W.nt + 1 + NW - 1) / NW), TB, 0, st>>>(w, n, avg, W, O);
     AK_LAUNCH_CHECK("k_build_split");
-    const size_t smem = sizeof(SecSmem<T>);
+    const size_t smem = sizeof(SecSmem);
     AK_CUDA_TRY(cudaFuncSetAttribute(k_build_pack<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
     k_build_pack<T><<<(unsigned)(W.nt + 1), TB, smem, st>>>(w, n, avg, W, O,

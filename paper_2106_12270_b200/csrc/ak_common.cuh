@@ -280,4 +280,40 @@ __device__ __forceinline__ void st_release_u32(u32 *p, u32 v)
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// mbarrier + 1-D bulk async copy (TMA engine) helpers
+__device__ __forceinline__ void mbar_init(u64 *bar, u32 count)
+{
+    u32 a = (u32)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(u64 *bar, u32 bytes)
+{
+    u32 a = (u32)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64 *bar, u32 phase)
+{
+    u32 a = (u32)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, u32 bytes, u64 *bar)
+{
+    u32 d = (u32)__cvta_generic_to_shared(dst);
+    u32 b = (u32)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(d),
+        "l"(src), "r"(bytes), "r"(b)
+        : "memory");
+}
+
 template <typename T> __device__ __forceinline__ double to_d(T v) { return (double)v; }

@@ -114,41 +114,6 @@ __global__ void k_rule_uniforms(const RowT *__restrict__ rows, double avg, i64 l
 // ---------------------------------------------------------------------------
 // sectioned sampler
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void mbar_init(u64 *bar, u32 count)
-{
-    u32 a = (u32)__cvta_generic_to_shared(bar);
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(u64 *bar, u32 bytes)
-{
-    u32 a = (u32)__cvta_generic_to_shared(bar);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(u64 *bar, u32 phase)
-{
-    u32 a = (u32)__cvta_generic_to_shared(bar);
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAIT_%=;\n"
-        "}\n" ::"r"(a),
-        "r"(phase)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, u32 bytes, u64 *bar)
-{
-    u32 d = (u32)__cvta_generic_to_shared(dst);
-    u32 b = (u32)__cvta_generic_to_shared(bar);
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(d),
-        "l"(src), "r"(bytes), "r"(b)
-        : "memory");
-}
-
 // Philox2x64-10 with a precomputed key schedule (the per-round keys depend
 // on the seed only, so they are hoisted out of the draw loop).
 struct KeySched64 {
@@ -354,7 +319,10 @@ __global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
         const int bb = pow2 ? __ffsll(span) - 1 : 0;
         const RowT *src = rows + lo;
         if (STAGE) {
-            __syncthreads();  // the previous section's rows are no longer read
+            // the previous section's rows are no longer read (generic proxy)
+            // before the async-proxy copy overwrites them
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
             const u32 bytes = (u32)(span * sizeof(RowT));
             if ((((uintptr_t)src) & 15) == 0 && (bytes & 15) == 0) {
                 if (threadIdx.x == 0) {

@@ -1,0 +1,42 @@
+"""Time psa_construct (CUDA events, device-resident weights) at one size.
+
+    python tools/time_build.py [--n 1e9] [--dist uniform|zipf] [--dtype float32|float64] [--reps 10]
+"""
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2106_12270_b200 as ak  # noqa: E402
+from paper_2106_12270_b200.pack import build_table  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=float, default=1e9)
+ap.add_argument("--dist", default="uniform")
+ap.add_argument("--dtype", default="float32")
+ap.add_argument("--reps", type=int, default=10)
+a = ap.parse_args()
+N = int(a.n)
+dt = torch.float32 if a.dtype == "float32" else torch.float64
+r = ak.RngStream(1)
+ws = ak.gen_uniform(N, r, dtype=dt) if a.dist == "uniform" else ak.gen_power_law(N, 1.0, r, dtype=dt)
+t = build_table(ws)
+for _ in range(3):
+    build_table(ws, t)
+torch.cuda.synchronize()
+ts = []
+for _ in range(a.reps):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    build_table(ws, t)
+    e1.record()
+    torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1))
+ts.sort()
+b = 4 if dt == torch.float32 else 8
+byts = N * (2 * b + b + 4)
+med = ts[len(ts) // 2]
+print(f"build N={N:.0e} {a.dist} {a.dtype}: median {med:.3f} ms  min {ts[0]:.3f} ms  "
+      f"{N / med / 1e6:.1f} G items/s  {byts / med / 1e6:.0f} GB/s algorithmic")
