@@ -185,13 +185,13 @@ __device__ __forceinline__ double warp_scan_mono(double x, int lane)
 // exclusive base within the chunk and the chunk total.
 template <bool LIGHT>
 __device__ __forceinline__ void lane_class(const double v[VV], double avg, double loc[VV], u32 &mask,
-                                           double &excl, double &total, int lane)
+                                           double &excl, double &total, int lane, bool full = false)
 {
     double s = 0.0;
     u32 m = 0;
 #pragma unroll
     for (int k = 0; k < VV; ++k) {
-        const bool valid = v[k] >= 0.0;
+        const bool valid = full || v[k] >= 0.0;
         const bool in = LIGHT ? (valid && v[k] <= avg) : (valid && v[k] > avg);
         if (LIGHT) loc[k] = s;
         if (in) s = s + (LIGHT ? (avg - v[k]) : (v[k] - avg));
@@ -619,7 +619,7 @@ __device__ __forceinline__ u32 warp_excl_count(u32 cnt, u32 &total, int lane)
 // pass-1 chunk bounds (8 lanes at once), the count inside the chunk from its
 // canonical keys.  Outputs: the boundary's heavy rank, the chunk holding that
 // rank, and the item of that heavy (the first heavy past the boundary).
-constexpr int HCAP = 1408;       // heavies per merge round (smem for 4 CTAs per SM)
+constexpr int HCAP = 1096;       // heavies per merge round (shared memory for 4 CTAs per SM)
 
 struct SplitOut {
     u64 *hrank;   // [nt+2]
@@ -749,11 +749,14 @@ __global__ void __launch_bounds__(TB) k_build_split(const T *__restrict__ w, u64
 // written directly: lights by the threads that own them, heavies in rank
 // order.  Large heavy ranges are processed in rounds of HCAP.
 struct SecSmem {
-    double LK[TILE + 1];           // own light keys (own frame), rank order; +inf sentinel
     u32 LS[TILE];                  // light successor heavy item (+1), 0 = unresolved
+    double LK[TILE + 2];           // own light keys (own frame), rank order; +inf sentinel
     dd HK[HCAP + 1];               // heavy keys (own frame); +inf sentinel
     u32 HI[HCAP + 1];              // heavy items; ~0 sentinel (LS = HI + 1 = 0: unresolved)
-    double SK[HCAP];               // heavy -> key of its successor light (+inf: none here)
+    double SK[HCAP];               // heavy -> key of its successor light (+inf: none here);
+                                   // before the merge: the heavy's key in its chunk frame
+    dd Dwin[32];                   // frame offset (chunk's tile base - own base) per window chunk
+    unsigned char CI[HCAP];        // window chunk of each heavy slot
     u32 lfirst;
     u64 next_item;                 // item of the heavy ranked jend (first of the next round)
 };
@@ -773,8 +776,6 @@ __device__ __forceinline__ void chunk_ranks(const BuildWs &W, u64 n, u64 g0, int
         const u32 a = __shfl_up_sync(0xffffffffu, inc, d);
         if (lane >= d) inc += a;
     }
-    // heavy rank of chunk g0's first heavy: heavies before its tile plus the
-    // heavies of the tile's earlier chunks
     const u64 t0 = g0 / NW;
     const int c0 = (int)(g0 % NW);
     u32 pre = 0;
@@ -783,6 +784,8 @@ __device__ __forceinline__ void chunk_ranks(const BuildWs &W, u64 n, u64 g0, int
     const u64 base = (g0 < nch ? heavies_before_tile(W, n, t0) : heavies_before_tile(W, n, W.nt)) + pre;
     hb = g < nch ? base + (inc - hc) : ~0ull;
 }
+
+__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7FF0000000000000ll); }
 
 template <typename T>
 __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u64 n, double avg,
@@ -803,6 +806,8 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
     const double secbound = u < nt ? W.mD[u * NW + NW - 1] : 0.0;  // next light key, own frame
 
     // ---- lights of tile u (rank order = key order), keys into shared memory
+    reinterpret_cast<uint4 *>(P.LS)[threadIdx.x] = make_uint4(0, 0, 0, 0);
+    reinterpret_cast<uint4 *>(P.LS)[threadIdx.x + TB] = make_uint4(0, 0, 0, 0);
     u32 nL = 0, lrank0 = 0, lm = 0;
     double lv[VV];
     if (u < nt) {
@@ -818,29 +823,25 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
         load8(w, n, u * TILE + (u64)wid * CH + (u64)lane * VV, lv);
         const double b0 = wid ? W.mD[u * NW + wid - 1] : 0.0, b1 = W.mD[u * NW + wid];
         double lk[VV], ex, tot;
-        lane_class<true>(lv, avg, lk, lm, ex, tot, lane);
+        lane_class<true>(lv, avg, lk, lm, ex, tot, lane, (u + 1) * TILE <= n);
         class_keys(lk, ex, b0, b1, lane);
         u32 tl;
         lrank0 = woff + warp_excl_count(__popc(lm), tl, lane);
-        u32 r = lrank0;
 #pragma unroll
         for (int q = 0; q < VV; ++q)
-            if ((lm >> q) & 1) {
-                P.LK[r] = lk[q];
-                P.LS[r] = 0;
-                ++r;
-            }
+            if ((lm >> q) & 1) P.LK[lrank0 + __popc(lm & ((1u << q) - 1))] = lk[q];
     }
-
-    if (threadIdx.x == 0) P.LK[nL] = __longlong_as_double(0x7FF0000000000000ll);
+    if (threadIdx.x == 0) {
+        P.LK[nL] = dinf();
+        P.next_item = NONE64;
+    }
+    __syncthreads();
 
     // ---- heavies in rounds of at most HCAP ranks (one round unless the
     // section's heavy range is large or spans more than 32 chunks)
     u64 jcur = J0;
     u64 gcur = O.hchunk[u];
     u32 lfirst = 0;  // first light not yet resolved
-    if (threadIdx.x == 0) P.next_item = NONE64;
-    __syncthreads();
     while (jcur < J1) {
         u64 hb;
         u32 hc;
@@ -850,49 +851,58 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
         if (last < jend) jend = last;
         const u32 nH = (u32)(jend - jcur);
         const bool last_round = jend >= J1;
-        // rebuild the chunks covering ranks [jcur, jend] (rank jend: the next
-        // round's first heavy), own frame
-        if (threadIdx.x == 0) {  // merge sentinels
-            P.HK[nH] = dd_make(__longlong_as_double(0x7FF0000000000000ll));
-            P.HI[nH] = 0xFFFFFFFFu;
+        const bool needed = hb != ~0ull && hb <= jend && hb + hc > jcur;
+        const unsigned need = __ballot_sync(0xffffffffu, needed);
+        if (wid == 0) {
+            // frame offset of each needed window chunk
+            if (needed) P.Dwin[lane] = dd_sub(W.DHb[(gcur + lane) / NW], own);
+            if (lane == 0) {  // merge sentinels
+                P.HK[nH] = dd_make(dinf());
+                P.HI[nH] = 0xFFFFFFFFu;
+            }
         }
-        const unsigned need = __ballot_sync(0xffffffffu, hb != ~0ull && hb <= jend && hb + hc > jcur);
+        // rebuild the needed chunks' heavy keys (chunk frame) into their
+        // rank slots; rank jend is the next round's first heavy
         for (int ci = wid; ci < 32; ci += NW) {
             if (!((need >> ci) & 1)) continue;
             const u64 cb = __shfl_sync(0xffffffffu, hb, ci);
             const u64 g = gcur + ci;
-            const u64 t = g / NW;
             const int c = (int)(g % NW);
             const double base = c ? W.mE[g - 1] : 0.0, bound = W.mE[g];
-            const dd D = dd_sub(W.DHb[t], own);
             double v[VV], k[VV], ex, tot;
             u32 m;
             load8(w, n, g * CH + (u64)lane * VV, v);
-            lane_class<false>(v, avg, k, m, ex, tot, lane);
+            lane_class<false>(v, avg, k, m, ex, tot, lane, (g + 1) * CH <= n);
             class_keys(k, ex, base, bound, lane);
             u32 tc;
-            u64 rr = cb + warp_excl_count(__popc(m), tc, lane);
+            const int r0 = (int)((i64)cb - (i64)jcur) + (int)warp_excl_count(__popc(m), tc, lane);
+            const u32 item0 = (u32)(g * CH + (u64)lane * VV);
 #pragma unroll
-            for (int q = 0; q < VV; ++q)
-                if ((m >> q) & 1) {
-                    const u32 item = (u32)(g * CH + (u64)lane * VV + q);
-                    if (rr >= jcur && rr < jend) {
-                        const u32 s = (u32)(rr - jcur);
-                        P.HK[s] = add_dd_d(D, k[q]);
-                        P.HI[s] = item;
-                    } else if (rr == jend) {
-                        P.next_item = item;
-                    }
-                    ++rr;
+            for (int q = 0; q < VV; ++q) {
+                const int sl = r0 + __popc(m & ((1u << q) - 1));
+                if (((m >> q) & 1) && sl >= 0 && sl < (int)nH) {
+                    P.SK[sl] = k[q];
+                    P.HI[sl] = item0 + q;
+                    P.CI[sl] = (unsigned char)ci;
                 }
+            }
+            const int want = (int)nH - r0;  // this lane holds rank jend?
+            if (want >= 0 && want < __popc(m)) {
+                u32 mm = m;
+                for (int z = 0; z < want; ++z) mm &= mm - 1;
+                P.next_item = item0 + (u32)(__ffs(mm) - 1);
+            }
         }
         __syncthreads();
+        // heavy keys into the own frame (double-double), one thread per heavy
+        for (u32 j = threadIdx.x; j < nH; j += TB) P.HK[j] = add_dd_d(P.Dwin[P.CI[j]], P.SK[j]);
         if (!last_round && wid == 0 && P.next_item == NONE64) {
             // rank jend lies past the enumerated chunks
             const u64 gl = gcur + 31;
             const u64 nx = next_heavy_after(W, gl / NW, (int)(gl % NW), lane);
             if (lane == 0) P.next_item = nx;
         }
+        __syncthreads();
         // merge path: lights [lfirst, nL) with heavies [0, nH); heavy first on
         // ties.  +inf sentinels end both lists; a taken heavy records the key
         // of its successor light, a taken light its successor heavy's item.
@@ -904,11 +914,41 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
             const u32 per = (total + TB - 1) / TB;
             const u32 d0 = threadIdx.x * per;
             if (d0 < total) {
-                u32 lo = d0 > nH ? d0 - nH : 0, hi = d0 < na ? d0 : na;
+                // lights among the first d0 merged: the greatest i with
+                // light i-1 before heavy d0-i (galloping from the
+                // proportional guess, then bisection)
+                const u32 lo0 = d0 > nH ? d0 - nH : 0, hi0 = d0 < na ? d0 : na;
+                auto light_first = [&](u32 i) {  // light i-1 precedes heavy d0-i
+                    return !le_dd_d(P.HK[d0 - i], LKp[i - 1]);
+                };
+                u32 g = total ? (u32)(((u64)d0 * na) / total) : 0;
+                g = g < lo0 ? lo0 : (g > hi0 ? hi0 : g);
+                u32 lo = lo0, hi = hi0;  // answer in [lo, hi]
+                if (g > lo0 && !light_first(g)) {
+                    hi = g - 1;
+                    u32 st = 1;
+                    while (true) {
+                        const u32 pnt = hi >= lo0 + st ? hi - st + 1 : lo0;
+                        if (pnt == lo0 || light_first(pnt)) { lo = pnt; break; }
+                        hi = pnt - 1;
+                        st <<= 1;
+                    }
+                } else {
+                    lo = g;
+                    u32 st = 1;
+                    while (true) {
+                        const u32 pnt = lo + st <= hi0 ? lo + st : hi0;
+                        if (pnt == lo) { hi = lo; break; }
+                        if (!light_first(pnt)) { hi = pnt - 1; break; }
+                        lo = pnt;
+                        if (pnt == hi0) { hi = hi0; break; }
+                        st <<= 1;
+                    }
+                }
                 while (lo < hi) {
-                    const u32 mid = (lo + hi) >> 1;
-                    if (!le_dd_d(P.HK[d0 - mid - 1], LKp[mid])) lo = mid + 1;
-                    else hi = mid;
+                    const u32 mid = (lo + hi + 1) >> 1;
+                    if (light_first(mid)) lo = mid;
+                    else hi = mid - 1;
                 }
                 u32 i = lo, j = d0 - lo;
                 const u32 steps = d0 + per < total ? per : total - d0;
@@ -933,7 +973,7 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
         for (u32 j = threadIdx.x; j < nH; j += TB) {
             const u32 item = P.HI[j];
             const double sk = P.SK[j];
-            const double DL = sk != __longlong_as_double(0x7FF0000000000000ll) ? sk : secbound;
+            const double DL = sk != dinf() ? sk : secbound;
             const dd tw = dd_add_d(add_dd_d(P.HK[j], -DL), avg);
             u64 al;
             if (j + 1 < nH) al = (u64)P.HI[j + 1] + 1;
@@ -966,18 +1006,17 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
     // lights: rows written by their owning lanes; unresolved ones alias the
     // first heavy past the section (or themselves)
     if (u < nt) {
-        u32 r = lrank0;
+        const u64 item0 = u * TILE + (u64)wid * CH + (u64)lane * VV;
+        const u64 dflt = after == NONE64 ? 0 : after + 1;  // 0: self
 #pragma unroll
         for (int q = 0; q < VV; ++q)
             if ((lm >> q) & 1) {
-                const u64 item = u * TILE + (u64)wid * CH + (u64)lane * VV + q;
-                const u32 s = P.LS[r];
-                const u64 al = s ? (u64)s : (after == NONE64 ? item + 1 : after + 1);
+                const u32 s = P.LS[lrank0 + __popc(lm & ((1u << q) - 1))];
+                const u64 al = s ? (u64)s : (dflt ? dflt : item0 + q + 1);
                 RowT row;
                 row.tw = (TwT)lv[q];
                 row.alias = (AliasT)al;
-                rows[item] = row;
-                ++r;
+                rows[item0 + q] = row;
             }
     }
 }

@@ -15,6 +15,10 @@
 // by the chi-square tests, not bit-compatible with the reference).
 #include "ak_common.cuh"
 
+#ifndef AK_FAST_ILP2
+#define AK_FAST_ILP2 0
+#endif
+
 namespace {
 
 // ---------------------------------------------------------------------------
@@ -222,42 +226,75 @@ __device__ __forceinline__ void store_pair(i64 *o0, i64 d0, i64 d1, bool v0, boo
 // cl0 + q, high word ch), its two 64-bit words are draws 2q and 2q + 1 of
 // ob.  Indices fit 32 bits (u32 aliases); outputs are written as int64 with
 // 16-byte stores (see store_pair for the misaligned case).
+// Philox4x32-10 with the round keys formed from the (warp-uniform) seed
+// words inline, so they live in uniform registers rather than per thread.
+__device__ __forceinline__ uint4 philox4x32_key(uint4 c, u32 k0, u32 k1)
+{
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const u32 hi0 = __umulhi(AK_PH4_M0, c.x), lo0 = AK_PH4_M0 * c.x;
+        const u32 hi1 = __umulhi(AK_PH4_M1, c.z), lo1 = AK_PH4_M1 * c.z;
+        c = make_uint4(hi1 ^ c.y ^ (k0 + (u32)r * AK_PH4_W0), lo1, hi0 ^ c.w ^ (k1 + (u32)r * AK_PH4_W1), lo0);
+    }
+    return c;
+}
+
+// the bucket rule for one 64-bit word on a staged f32 section of span 2^b
+__device__ __forceinline__ u32 rule_f32_pow2(const RowF32 *tab, u32 wl, u32 wh, int sk, int b,
+                                             u64 fmask, u32 lo1, double avg)
+{
+    const u64 word = ((u64)wh << 32) | wl;
+    const u32 k = wh >> sk;
+    const u64 f = (word >> 11) & fmask;
+    const double frac = __longlong_as_double((long long)(0x3FF0000000000000ull | (f << (b - 1)))) - 1.0;
+    const uint2 row = *reinterpret_cast<const uint2 *>(tab + k);
+    return (frac * avg < (double)__uint_as_float(row.x)) ? lo1 + k : row.y;
+}
+
+__device__ __forceinline__ void store_pair_fast(i64 *p, u32 d0, u32 d1, int par, int lane)
+{
+    if (par == 0) {
+        *reinterpret_cast<longlong2 *>(p) = make_longlong2((long long)d0, (long long)d1);
+    } else {
+        const u32 nx = __shfl_down_sync(0xffffffffu, d0, 1);
+        if (lane < 31) *reinterpret_cast<longlong2 *>(p + 1) = make_longlong2((long long)d1, (long long)nx);
+        else p[1] = (i64)d1;
+        if (lane == 0) p[0] = (i64)d0;
+    }
+}
+
+// Fast-mode interior of a section (f32 rows staged in shared memory, span
+// 2^b): pairs q in [qa, qb) with qb - qa a multiple of the CTA size, every
+// draw in range.  Pair q is one Philox4x32-10 call (counter low word
+// cl0 + q, high word ch), its two 64-bit words are draws 2q and 2q + 1 of
+// ob.  Indices fit 32 bits (u32 aliases); outputs are written as int64 with
+// 16-byte stores (see store_pair for the misaligned case).  Two calls are
+// interleaved per thread for instruction-level parallelism.
 __device__ __forceinline__ void fast_pairs_f32(const RowF32 *tab, u32 cl0, u32 ch, u64 strm,
-                                               const KeySched32 &ks, i64 *ob, u32 qa, u32 qb,
+                                               u64 seed, i64 *ob, u32 qa, u32 qb,
                                                int b, u32 lo1, double avg, int par, int lane)
 {
     const u32 sl = (u32)strm, sh = (u32)(strm >> 32);
+    const u32 k0 = (u32)seed, k1 = (u32)(seed >> 32);
     const int sk = 32 - b;
     const u64 fmask = (1ull << (53 - b)) - 1;
-    for (u32 q = qa + threadIdx.x; q < qb; q += blockDim.x) {
-        uint4 c = make_uint4(cl0 + q, ch, sl, sh);
-#pragma unroll
-        for (int r = 0; r < 10; ++r) {
-            const u32 hi0 = __umulhi(AK_PH4_M0, c.x), lo0 = AK_PH4_M0 * c.x;
-            const u32 hi1 = __umulhi(AK_PH4_M1, c.z), lo1_ = AK_PH4_M1 * c.z;
-            c = make_uint4(hi1 ^ c.y ^ ks.k[r].x, lo1_, hi0 ^ c.w ^ ks.k[r].y, lo0);
-        }
-        u32 d[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const u32 wl = h ? c.z : c.x, wh = h ? c.w : c.y;
-            const u64 word = ((u64)wh << 32) | wl;
-            const u32 k = wh >> sk;
-            const u64 f = (word >> 11) & fmask;
-            const double frac =
-                __longlong_as_double((long long)(0x3FF0000000000000ull | (f << (b - 1)))) - 1.0;
-            const uint2 row = *reinterpret_cast<const uint2 *>(tab + k);
-            d[h] = (frac * avg < (double)__uint_as_float(row.x)) ? lo1 + k : row.y;
-        }
-        i64 *p = ob + 2 * (u64)q;
-        if (par == 0) {
-            *reinterpret_cast<longlong2 *>(p) = make_longlong2((long long)d[0], (long long)d[1]);
-        } else {
-            const u32 nx = __shfl_down_sync(0xffffffffu, d[0], 1);
-            if (lane < 31) *reinterpret_cast<longlong2 *>(p + 1) = make_longlong2((long long)d[1], (long long)nx);
-            else p[1] = (i64)d[1];
-            if (lane == 0) p[0] = (i64)d[0];
-        }
+    const u32 step = blockDim.x;
+    u32 q = qa + threadIdx.x;
+#if AK_FAST_ILP2
+    // (qb - qa) is a multiple of blockDim: every thread runs the same trips
+    for (; q + step < qb; q += 2 * step) {
+        const uint4 c0 = philox4x32_key(make_uint4(cl0 + q, ch, sl, sh), k0, k1);
+        const uint4 c1 = philox4x32_key(make_uint4(cl0 + q + step, ch, sl, sh), k0, k1);
+        store_pair_fast(ob + 2 * (u64)q, rule_f32_pow2(tab, c0.x, c0.y, sk, b, fmask, lo1, avg),
+                        rule_f32_pow2(tab, c0.z, c0.w, sk, b, fmask, lo1, avg), par, lane);
+        store_pair_fast(ob + 2 * (u64)(q + step), rule_f32_pow2(tab, c1.x, c1.y, sk, b, fmask, lo1, avg),
+                        rule_f32_pow2(tab, c1.z, c1.w, sk, b, fmask, lo1, avg), par, lane);
+    }
+#endif
+    for (; q < qb; q += step) {
+        const uint4 c0 = philox4x32_key(make_uint4(cl0 + q, ch, sl, sh), k0, k1);
+        store_pair_fast(ob + 2 * (u64)q, rule_f32_pow2(tab, c0.x, c0.y, sk, b, fmask, lo1, avg),
+                        rule_f32_pow2(tab, c0.z, c0.w, sk, b, fmask, lo1, avg), par, lane);
     }
 }
 
@@ -286,8 +323,6 @@ __global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const KeySched64 ks64 = sched64(seed);
-    const KeySched32 ks32 = sched32(seed);
     // this CTA's slice of the pass's draw space
     const u64 last = first + count - 1;
     const i64 Dbeg = offsets[first];
@@ -355,10 +390,15 @@ __global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
                 const bool v1 = p <= pe && i0 + 1 >= ia && i0 + 1 < ib;
                 u64 w0, w1;
                 if (MODE == AK_RNG_REFERENCE) {
-                    w0 = philox64_sched(ctr0 + (u64)i0, strm, ks64);
-                    w1 = philox64_sched(ctr0 + (u64)i0 + 1, strm, ks64);
+                    w0 = ak_philox2x64_10(ctr0 + (u64)i0, strm, seed, nullptr);
+                    w1 = ak_philox2x64_10(ctr0 + (u64)i0 + 1, strm, seed, nullptr);
                 } else {
-                    philox32_sched(((ctr0 + (u64)i0) >> 1), strm, ks32, w0, w1);
+                    const u64 call = (ctr0 + (u64)i0) >> 1;
+                    const uint4 c = philox4x32_key(make_uint4((u32)call, (u32)(call >> 32), (u32)strm,
+                                                              (u32)(strm >> 32)),
+                                                   (u32)seed, (u32)(seed >> 32));
+                    w0 = ((u64)c.y << 32) | c.x;
+                    w1 = ((u64)c.w << 32) | c.z;
                 }
                 const i64 d0 = rule_word(tab, w0, span, bb, pow2, (i64)lo, avg);
                 const i64 d1 = rule_word(tab, w1, span, bb, pow2, (i64)lo, avg);
@@ -377,7 +417,7 @@ __global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
             if (nfast > 0) {
                 if (qa > 0) generic(p0, p0 + qa - 1);
                 fast_pairs_f32(reinterpret_cast<const RowF32 *>(tab), (u32)cb, (u32)(cb >> 32),
-                               strm, ks32, o + (2 * p0 - poff), (u32)qa, (u32)(qa + nfast), bb,
+                               strm, seed, o + (2 * p0 - poff), (u32)qa, (u32)(qa + nfast), bb,
                                (u32)(lo + 1), avg, par, lane);
                 if (qa + nfast < np) generic(p0 + qa + nfast, p1);
                 continue;
