@@ -142,9 +142,34 @@ size_t ak_build_workspace_bytes(uint64_t n, int dtype);
  * readable afterwards with ak_build_stats. */
 int ak_build_psa(const void *w, int dtype, uint64_t n, double total, void *rows, void *ws,
                  size_t ws_bytes, void *stream);
+/* ak_build_psa with the bucket size avg given instead of total/n (the PSA+
+ * residual is built with the global average, pack.py:297-299). */
+int ak_build_psa_avg(const void *w, int dtype, uint64_t n, double avg, void *rows, void *ws,
+                     size_t ws_bytes, void *stream);
 /* [sync] Light/heavy counts and tile count of the last ak_build_psa on ws. */
 int ak_build_stats(const void *ws, uint64_t n, uint64_t *nl, uint64_t *nh, uint64_t *tiles,
                    void *stream);
+
+/* ---- PSA+ (greedy_prepack, partition.py:134-282; pack.py:280-305) ------- */
+
+size_t ak_prepack_workspace_bytes(uint64_t n, uint32_t block_size);
+/* [sync] _greedy_kernel (partition.py:134-227): per block of block_size items,
+ * exactly-full items fill their own rows; if the block holds >= threshold
+ * lights (w < avg) and heavies (w > avg) they are paired by the block-local
+ * sequential order until one side runs out.  `rows` (table layout of dtype,
+ * zeroed here) gets every handled row; the leftovers, in item order, go to
+ * res_idx (1-based) / res_w (f64; the partially consumed heavy carries its
+ * residual); *nres_out / *nwritten_out their counts.  Replaces the
+ * _greedy_kernel_nb call (partition.py:253). */
+int ak_greedy_prepack(const void *w, int dtype, uint64_t n, double avg, uint32_t block_size,
+                      uint32_t threshold, void *rows, int64_t *res_idx, double *res_w,
+                      uint64_t *nres_out, uint64_t *nwritten_out, void *ws, size_t ws_bytes,
+                      void *stream);
+/* The residual's table (f64 rows over residual positions 1..nres, built with
+ * ak_build_psa_avg on res_w) written into the final table at res_idx, aliases
+ * mapped back to item ids (pack.py:297-299). */
+int ak_residual_scatter(const void *res_rows, const int64_t *res_idx, uint64_t nres, double avg,
+                        int dtype, void *rows, void *stream);
 
 /* ---- sampling (sample.py) ----------------------------------------------- */
 

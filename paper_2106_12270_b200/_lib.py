@@ -45,6 +45,11 @@ _SIGS = {
     "ak_build_workspace_bytes": (sz, [u64, ci]),
     "ak_build_psa": (ci, [vp, ci, u64, dbl, vp, vp, sz, vp]),
     "ak_build_stats": (ci, [vp, u64, vp, vp, vp, vp]),
+    "ak_build_psa_avg": (ci, [vp, ci, u64, dbl, vp, vp, sz, vp]),
+    "ak_prepack_workspace_bytes": (sz, [u64, C.c_uint32]),
+    "ak_greedy_prepack": (ci, [vp, ci, u64, dbl, C.c_uint32, C.c_uint32, vp, vp, vp, vp, vp, vp,
+                               sz, vp]),
+    "ak_residual_scatter": (ci, [vp, vp, u64, dbl, ci, vp, vp]),
     "ak_sample_naive": (ci, [vp, ci, u64, dbl, u64, u64, u64, u64, u64, u64, vp, ci, vp]),
     "ak_sample_from_uniforms": (ci, [vp, ci, u64, dbl, u64, u64, vp, u64, vp, vp]),
     "ak_num_sections": (u64, [u64, u64]),

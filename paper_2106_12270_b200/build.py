@@ -23,7 +23,8 @@ ROOT = os.path.dirname(HERE)
 OBJ = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "libaliaskit_b200.so")
 
-CU_SOURCES = ["ak_sample.cu", "ak_weights.cu", "ak_partition.cu", "ak_build.cu", "ak_verify.cu"]
+CU_SOURCES = ["ak_sample.cu", "ak_weights.cu", "ak_partition.cu", "ak_build.cu", "ak_verify.cu",
+              "ak_prepack.cu"]
 CPP_SOURCES = ["ak_host.cpp"]
 HEADERS = ["ak_common.cuh"]
 

@@ -1022,11 +1022,10 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
 }
 
 template <typename T>
-int run_build(const void *wv, u64 n, double total, void *rows, void *ws, cudaStream_t st)
+int run_build(const void *wv, u64 n, double avg, void *rows, void *ws, cudaStream_t st)
 {
     const T *w = (const T *)wv;
     BuildWs W = carve(ws, n);
-    const double avg = total / (double)n;
     SplitOut O;
     {
         char *tail = (char *)ws + ws_bytes_for(n) - split_bytes(n);
@@ -1066,17 +1065,23 @@ size_t ak_build_workspace_bytes(uint64_t n, int dtype)
 int ak_build_psa(const void *w, int dtype, uint64_t n, double total, void *rows, void *ws,
                  size_t ws_bytes, void *stream)
 {
+    return ak_build_psa_avg(w, dtype, n, total / (double)n, rows, ws, ws_bytes, stream);
+}
+
+int ak_build_psa_avg(const void *w, int dtype, uint64_t n, double avg, void *rows, void *ws,
+                     size_t ws_bytes, void *stream)
+{
     if (n == 0) return AK_ERR_EMPTY_INPUT;
     if (ws_bytes < ws_bytes_for(n)) return AK_ERR_WORKSPACE;
     if (((uintptr_t)w & 15) != 0 || ((uintptr_t)rows & 15) != 0) return AK_ERR_VALUE;
     cudaStream_t st = ak_stream(stream);
     if (dtype == AK_F32) {
         if (n >= 0xFFFFFFFFull) return AK_ERR_VALUE;  // u32 aliases
-        return run_build<float>(w, n, total, rows, ws, st);
+        return run_build<float>(w, n, avg, rows, ws, st);
     }
     if (dtype == AK_F64) {
         if (n >= 0xFFFFFFFFull) return AK_ERR_VALUE;  // u32 item ids in the pack windows
-        return run_build<double>(w, n, total, rows, ws, st);
+        return run_build<double>(w, n, avg, rows, ws, st);
     }
     return AK_ERR_VALUE;
 }

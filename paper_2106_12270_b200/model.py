@@ -85,8 +85,8 @@ class AliasTable:
             return self.rows.view(torch.int32)[1::2].to(torch.int64) & 0xFFFFFFFF
         return self.rows.view(self.n, 2)[:, 1]
 
-    def to_numpy(self) -> tuple[np.ndarray, np.ndarray]:
-        """(tw float64[N], alias int64[N]) on the host: the reference layout."""
+    def tw_alias(self) -> tuple[torch.Tensor, torch.Tensor]:
+        """(tw float64[N], alias int64[N]) on the device: the reference layout."""
         tw = torch.empty(self.n, dtype=torch.float64, device=self.rows.device)
         al = torch.empty(self.n, dtype=torch.int64, device=self.rows.device)
         with torch.cuda.device(self.rows.device):
@@ -94,7 +94,23 @@ class AliasTable:
                                                  _lib.ptr(tw), _lib.ptr(al),
                                                  _lib.stream_ptr(self.rows.device)),
                        "rows_to_soa")
+        return tw, al
+
+    def to_numpy(self) -> tuple[np.ndarray, np.ndarray]:
+        """(tw float64[N], alias int64[N]) on the host: the reference layout."""
+        tw, al = self.tw_alias()
         return tw.cpu().numpy(), al.cpu().numpy()
+
+    def count_unwritten(self) -> int:
+        """Rows with alias 0 (the pack.py:275-276 check)."""
+        import ctypes as C
+
+        un = C.c_uint64(0)
+        with torch.cuda.device(self.rows.device):
+            _lib.check(_lib.lib().ak_count_unwritten(_lib.ptr(self.rows), self.dtype_code, self.n,
+                                                     C.byref(un), _lib.stream_ptr(self.rows.device)),
+                       "count_unwritten")
+        return int(un.value)
 
     @property
     def rows_list(self) -> list[tuple[float, int]]:

@@ -1,0 +1,139 @@
+"""GPU parity of PSA+ (greedy_prepack, partition.py:134-282; psa_plus_construct,
+pack.py:280-305) against the golden fixtures and the oracle's restatement.
+
+Contract: the block-local pairing is the reference's sequential order
+computed from block-local prefix keys, so handled rows, the forwarded
+residual (items and weights) and the handled fraction equal the reference's
+except at ties inside the reference's own f64 rounding (integer weights,
+exactly-avg residuals); thresholds within 1e-9*avg; the final PSA+ table
+equals the oracle composition (prepack + split plan + pack on the residual)
+the same way and passes validate_table.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2106_12270_b200 as ak
+from conftest import random_weights
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def oracle_psa_plus(w, tot, s, bs, thr):
+    """pack.py:280-305 composed from the oracle's restatements."""
+    pre = O.greedy_prepack(w, tot, bs, thr)
+    tw, alias = pre["tw"].copy(), pre["alias"].copy()
+    lm = pre["res_light"] == 1
+    part = dict(l_index=pre["res_idx"][lm].copy(), l_weight=pre["res_w"][lm].copy(),
+                h_index=pre["res_idx"][~lm].copy(), h_weight=pre["res_w"][~lm].copy(),
+                avg=tot / w.size)
+    part["lprefix"] = O.exclusive_prefix(part["l_weight"])
+    part["hprefix"] = O.exclusive_prefix(part["h_weight"])
+    nres = pre["res_idx"].size
+    if nres:
+        se = min(s, nres)
+        lc, hc, sp = O.compute_split_plan(part["lprefix"], part["hprefix"], part["h_weight"],
+                                          nres, se, part["avg"])
+        O.pack_sections(part, lc, hc, sp, 1, se, tw, alias)
+    return pre, tw, alias
+
+
+def check_prepack(w, bs, thr, tie_ok=False):
+    ws = ak.make_weight_set(w)
+    w64 = ws.weights.double().cpu().numpy()
+    ref = O.greedy_prepack(w64, ws.total, bs, thr)
+    got = ak.greedy_prepack(ws, block_size=bs, min_pair_threshold=thr)
+    al = got.alias.cpu().numpy()
+    tw = got.tw.cpu().numpy()
+    diff = np.count_nonzero(al != ref["alias"])
+    if tie_ok:
+        assert diff <= max(8, w64.size // 100), diff
+    else:
+        assert diff == 0, diff
+        assert got.handled_fraction == ref["nwritten"] / w64.size
+        same = ref["alias"] != 0
+        assert np.max(np.abs(tw[same] - ref["tw"][same]), initial=0.0) <= 1e-9 * ws.average
+        r = got.residual
+        idx = np.concatenate([r.l_index.cpu().numpy(), r.h_index.cpu().numpy()])
+        wts = np.concatenate([r.l_weight.cpu().numpy(), r.h_weight.cpu().numpy()])
+        o = np.argsort(idx)
+        assert np.array_equal(idx[o], ref["res_idx"])
+        assert np.max(np.abs(wts[o] - ref["res_w"]), initial=0.0) <= 1e-9 * ws.average
+    return got, ref
+
+
+def test_golden_prepack(golden):
+    for ci in range(len(golden["sizes"])):
+        k = f"c{ci}_"
+        w = golden[k + "weights"]
+        ws = ak.make_weight_set(w)
+        got = ak.greedy_prepack(ws, block_size=64, min_pair_threshold=4)
+        al = got.alias.cpu().numpy()
+        diff = np.count_nonzero(al != golden[k + "pre_alias"])
+        if ci % 5 == 3:  # integer weights: exact real ties
+            assert diff <= max(8, w.size // 100)
+            continue
+        assert diff == 0, ci
+        assert got.handled_fraction == float(golden[k + "pre_handled"][0])
+        assert np.array_equal(got.residual.l_index.cpu().numpy(), golden[k + "pre_res_l"])
+        assert np.array_equal(got.residual.h_index.cpu().numpy(), golden[k + "pre_res_h"])
+        assert np.allclose(got.residual.h_weight.cpu().numpy(), golden[k + "pre_res_hw"],
+                           rtol=0, atol=1e-9 * ws.average)
+
+
+@pytest.mark.parametrize("bs,thr", [(2, 1), (7, 2), (64, 4), (4096, 8), (1000, 300)])
+def test_random_prepack_vs_oracle(rng, bs, thr):
+    for trial in range(10):
+        n = int(np.exp(rng.uniform(0, np.log(200_000)))) + 1
+        w = random_weights(rng, n, trial % 5)
+        check_prepack(w, bs, thr, tie_ok=trial % 5 == 3)
+
+
+def test_exact_avg_items_and_edges():
+    # exactly-full items fill their own rows; tiny blocks; all-equal weights
+    for w in ([2.0] * 100, [1.0, 3.0] * 50, [1.0, 2.0, 3.0] * 33 + [2.0], [5.0]):
+        check_prepack(np.asarray(w, dtype=np.float64), 4, 1)
+    with pytest.raises(ValueError):
+        ak.greedy_prepack(ak.make_weight_set([1.0, 2.0]), block_size=1)
+    with pytest.raises(ValueError):
+        ak.greedy_prepack(ak.make_weight_set([1.0, 2.0]), min_pair_threshold=0)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_psa_plus_vs_oracle(rng, dtype):
+    for trial in range(12):
+        n = int(np.exp(rng.uniform(1, np.log(300_000)))) + 1
+        w = random_weights(rng, n, trial % 5)
+        if dtype == torch.float32:
+            w = w.astype(np.float32)
+        ws = ak.make_weight_set(torch.from_numpy(np.ascontiguousarray(w)).to(DEV))
+        w64 = ws.weights.double().cpu().numpy()
+        bs = int(rng.choice([64, 512, 4096]))
+        t = ak.psa_plus_construct(ws, s=64, block_size=bs, threshold=8)
+        pre, rtw, ral = oracle_psa_plus(w64, ws.total, 64, bs, 8)
+        tw, al = t.to_numpy()
+        diff = np.count_nonzero(al != ral)
+        if trial % 5 == 3:
+            assert diff <= max(8, n // 100)
+        else:
+            assert diff == 0, (n, bs, trial % 5)
+            same = al == ral
+            tol = 1e-9 if dtype == torch.float64 else 1e-6
+            assert np.max(np.abs(tw - rtw)[same]) <= tol * ws.average
+        rep = ak.validate_table(t, ws, tol=1e-9 if dtype == torch.float64 else 1e-4)
+        assert rep.ok, rep
+
+
+def test_psa_plus_large_handled_fraction(acceptance):
+    """c9-style gate (test_acceptance.py:262-272): most items are handled by
+    the block pass, and the table is valid."""
+    ws = ak.gen_uniform(10**7, ak.RngStream(seed=3))
+    pre = ak.greedy_prepack(ws)
+    t = ak.psa_plus_construct(ws)
+    rep = ak.validate_table(t, ws, tol=1e-9)
+    ok = pre.handled_fraction >= 0.5 and rep.ok
+    acceptance(f"{'PASS' if ok else 'FAIL'}  PSA+ N=1e7 uniform: handled {pre.handled_fraction:.4f}, {rep}")
+    assert ok
