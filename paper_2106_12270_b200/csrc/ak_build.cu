@@ -1003,21 +1003,34 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
         jcur = jend;
         __syncthreads();
     }
-    // lights: rows written by their owning lanes; unresolved ones alias the
-    // first heavy past the section (or themselves)
+    // lights: unresolved ones alias the first heavy past the section (or
+    // themselves).  The light keys are no longer needed: their space maps
+    // each tile position to its light rank, so that consecutive threads write
+    // consecutive rows (8 sectors per warp store instead of 32).
     if (u < nt) {
-        const u64 item0 = u * TILE + (u64)wid * CH + (u64)lane * VV;
-        const u64 dflt = after == NONE64 ? 0 : after + 1;  // 0: self
+        unsigned short *LR = reinterpret_cast<unsigned short *>(P.LK);
+        __syncthreads();  // every light key read (merge) before the space is reused
+        const u32 p0 = wid * CH + lane * VV;
 #pragma unroll
         for (int q = 0; q < VV; ++q)
-            if ((lm >> q) & 1) {
-                const u32 s = P.LS[lrank0 + __popc(lm & ((1u << q) - 1))];
-                const u64 al = s ? (u64)s : (dflt ? dflt : item0 + q + 1);
+            LR[p0 + q] = ((lm >> q) & 1) ? (unsigned short)(lrank0 + __popc(lm & ((1u << q) - 1)))
+                                         : (unsigned short)0xFFFFu;
+        __syncthreads();
+        const u64 t0 = u * TILE;
+        const u64 dflt = after == NONE64 ? 0 : after + 1;  // 0: self
+#pragma unroll
+        for (int k = 0; k < TILE / TB; ++k) {
+            const u32 p = k * TB + threadIdx.x;
+            const u32 r = LR[p];
+            if (r != 0xFFFFu) {
+                const u32 s = P.LS[r];
+                const u64 al = s ? (u64)s : (dflt ? dflt : t0 + p + 1);
                 RowT row;
-                row.tw = (TwT)lv[q];
+                row.tw = (TwT)w[t0 + p];
                 row.alias = (AliasT)al;
-                rows[item0 + q] = row;
+                rows[t0 + p] = row;
             }
+        }
     }
 }
 
