@@ -619,7 +619,7 @@ __device__ __forceinline__ u32 warp_excl_count(u32 cnt, u32 &total, int lane)
 // pass-1 chunk bounds (8 lanes at once), the count inside the chunk from its
 // canonical keys.  Outputs: the boundary's heavy rank, the chunk holding that
 // rank, and the item of that heavy (the first heavy past the boundary).
-constexpr int HCAP = 1096;       // heavies per merge round (shared memory for 4 CTAs per SM)
+constexpr int HCAP = 1472;       // heavies per merge round (shared memory for 4 CTAs per SM)
 
 struct SplitOut {
     u64 *hrank;   // [nt+2]
@@ -748,18 +748,32 @@ __global__ void __launch_bounds__(TB) k_build_split(const T *__restrict__ w, u64
 // light its successor heavy and each heavy its successor light; rows are
 // written directly: lights by the threads that own them, heavies in rank
 // order.  Large heavy ranges are processed in rounds of HCAP.
+// Keys in shared memory are order-preserving 64-bit integers: for a key
+// x >= 0, enc(x) = bits(x) << 1 (non-negative doubles order like their bit
+// patterns); a heavy's double-double key (hi, lo) becomes
+// (bits(hi) << 1) | (lo > 0), so "heavy <= light" (heavy first on ties) is
+// one unsigned compare and exact against the double light keys.
 struct SecSmem {
     u32 LS[TILE];                  // light successor heavy item (+1), 0 = unresolved
-    double LK[TILE + 2];           // own light keys (own frame), rank order; +inf sentinel
-    dd HK[HCAP + 1];               // heavy keys (own frame); +inf sentinel
+    u64 LK[TILE + 2];              // own light keys (own frame, encoded), rank order; ~0 sentinel
+    u64 HK[HCAP + 1];              // heavy keys (own frame, encoded); ~0 sentinel
     u32 HI[HCAP + 1];              // heavy items; ~0 sentinel (LS = HI + 1 = 0: unresolved)
-    double SK[HCAP];               // heavy -> key of its successor light (+inf: none here);
-                                   // before the merge: the heavy's key in its chunk frame
+    u64 SK[HCAP];                  // heavy -> encoded key of its successor light (~0: none
+                                   // here); before the merge: the heavy's key in its chunk
+                                   // frame (a double)
     dd Dwin[32];                   // frame offset (chunk's tile base - own base) per window chunk
     unsigned char CI[HCAP];        // window chunk of each heavy slot
     u32 lfirst;
     u64 next_item;                 // item of the heavy ranked jend (first of the next round)
 };
+
+__device__ __forceinline__ u64 key_enc(double x) { return (u64)__double_as_longlong(x) << 1; }
+__device__ __forceinline__ u64 key_enc_dd(dd x)
+{
+    return ((u64)__double_as_longlong(x.hi) << 1) | (x.lo > 0.0 ? 1ull : 0ull);
+}
+__device__ __forceinline__ double key_dec(u64 e) { return __longlong_as_double((long long)(e >> 1)); }
+constexpr u64 KEY_INF = ~0ull;
 
 // heavy rank of the first heavy of each of the 32 chunks g0 .. g0+31 (lane
 // i holds chunk g0 + i; ~0 past the last chunk) and its heavy count; every
@@ -829,10 +843,10 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
         lrank0 = woff + warp_excl_count(__popc(lm), tl, lane);
 #pragma unroll
         for (int q = 0; q < VV; ++q)
-            if ((lm >> q) & 1) P.LK[lrank0 + __popc(lm & ((1u << q) - 1))] = lk[q];
+            if ((lm >> q) & 1) P.LK[lrank0 + __popc(lm & ((1u << q) - 1))] = key_enc(lk[q]);
     }
     if (threadIdx.x == 0) {
-        P.LK[nL] = dinf();
+        P.LK[nL] = KEY_INF;
         P.next_item = NONE64;
     }
     __syncthreads();
@@ -857,7 +871,7 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
             // frame offset of each needed window chunk
             if (needed) P.Dwin[lane] = dd_sub(W.DHb[(gcur + lane) / NW], own);
             if (lane == 0) {  // merge sentinels
-                P.HK[nH] = dd_make(dinf());
+                P.HK[nH] = KEY_INF;
                 P.HI[nH] = 0xFFFFFFFFu;
             }
         }
@@ -881,7 +895,7 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
             for (int q = 0; q < VV; ++q) {
                 const int sl = r0 + __popc(m & ((1u << q) - 1));
                 if (((m >> q) & 1) && sl >= 0 && sl < (int)nH) {
-                    P.SK[sl] = k[q];
+                    P.SK[sl] = (u64)__double_as_longlong(k[q]);
                     P.HI[sl] = item0 + q;
                     P.CI[sl] = (unsigned char)ci;
                 }
@@ -895,7 +909,8 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
         }
         __syncthreads();
         // heavy keys into the own frame (double-double), one thread per heavy
-        for (u32 j = threadIdx.x; j < nH; j += TB) P.HK[j] = add_dd_d(P.Dwin[P.CI[j]], P.SK[j]);
+        for (u32 j = threadIdx.x; j < nH; j += TB)
+            P.HK[j] = key_enc_dd(add_dd_d(P.Dwin[P.CI[j]], __longlong_as_double((long long)P.SK[j])));
         if (!last_round && wid == 0 && P.next_item == NONE64) {
             // rank jend lies past the enumerated chunks
             const u64 gl = gcur + 31;
@@ -907,7 +922,7 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
         // ties.  +inf sentinels end both lists; a taken heavy records the key
         // of its successor light, a taken light its successor heavy's item.
         {
-            const double *LKp = P.LK + lfirst;
+            const u64 *LKp = P.LK + lfirst;
             u32 *LSp = P.LS + lfirst;
             const u32 na = nL - lfirst;
             const u32 total = na + nH;
@@ -919,7 +934,7 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
                 // proportional guess, then bisection)
                 const u32 lo0 = d0 > nH ? d0 - nH : 0, hi0 = d0 < na ? d0 : na;
                 auto light_first = [&](u32 i) {  // light i-1 precedes heavy d0-i
-                    return !le_dd_d(P.HK[d0 - i], LKp[i - 1]);
+                    return P.HK[d0 - i] > LKp[i - 1];
                 };
                 u32 g = total ? (u32)(((u64)d0 * na) / total) : 0;
                 g = g < lo0 ? lo0 : (g > hi0 ? hi0 : g);
@@ -952,10 +967,10 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
                 }
                 u32 i = lo, j = d0 - lo;
                 const u32 steps = d0 + per < total ? per : total - d0;
-                double lk = LKp[i];
-                dd hk = P.HK[j];
+                u64 lk = LKp[i];
+                u64 hk = P.HK[j];
                 for (u32 d = 0; d < steps; ++d) {
-                    if (le_dd_d(hk, lk)) {
+                    if (hk <= lk) {
                         P.SK[j] = lk;
                         ++j;
                         hk = P.HK[j];
@@ -972,14 +987,14 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
         const u64 nxt = last_round ? after : P.next_item;
         for (u32 j = threadIdx.x; j < nH; j += TB) {
             const u32 item = P.HI[j];
-            const double sk = P.SK[j];
-            const double DL = sk != dinf() ? sk : secbound;
-            const dd tw = dd_add_d(add_dd_d(P.HK[j], -DL), avg);
+            const u64 sk = P.SK[j];
+            const double DL = sk != KEY_INF ? key_dec(sk) : secbound;
+            const double tw = (key_dec(P.HK[j]) - DL) + avg;
             u64 al;
             if (j + 1 < nH) al = (u64)P.HI[j + 1] + 1;
             else al = nxt == NONE64 ? (u64)item + 1 : nxt + 1;
             RowT row;
-            row.tw = tw_store<T>(tw.hi + tw.lo, avg);
+            row.tw = tw_store<T>(tw, avg);
             row.alias = (AliasT)al;
             rows[item] = row;
         }
