@@ -381,9 +381,9 @@ __global__ void __launch_bounds__(SC_WARPS * 32) k_build_scan(const T *__restric
 #pragma unroll
                 for (int q = 0; q < VV; ++q) {
                     const bool li = v[q] <= avgT;
-                    const double dv = (double)v[q];
-                    xl[q] = li ? avg - dv : 0.0;
-                    xh[q] = li ? 0.0 : dv - avg;
+                    const double x = (double)v[q] - avg;  // avg - w == -(w - avg) exactly
+                    xl[q] = li ? -x : 0.0;
+                    xh[q] = li ? 0.0 : x;
                     lm |= (u32)li << q;
                 }
                 vm = 0xFFu;
