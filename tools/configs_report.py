@@ -1,0 +1,117 @@
+"""Every BASELINE.json config on one B200: time, algorithmic bytes and the
+fraction of the measured HBM copy bandwidth, with a parity spot check.
+
+    python tools/configs_report.py [--json out.json]
+
+C1  N=1e6 uniform f64: PSA construction + 1e6 naive samples
+C2  N=1e8 uniform f32: construction + 1e9 naive samples
+C3  N=1e8 shuffled power law (alpha=1) f32 (and f64): construction
+C4  N=1e9 f32 table: one pass of batched/sectioned sampling (the bench's)
+C5  N=1e9 uniform f64 (and f32): construction
+Algorithmic bytes: build N(2 b_w + b_row); naive M(b_row + 8);
+sectioned M*8 + rows of the sections drawn.
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2106_12270_b200 as ak  # noqa: E402
+from paper_2106_12270_b200.pack import build_table  # noqa: E402
+from paper_2106_12270_b200.sample import sectioned_sample_into  # noqa: E402
+
+PEAK = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                   "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+    os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) else 6650.0
+
+
+def timed(fn, reps=5):
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return sorted(ts)[len(ts) // 2] / 1e3
+
+
+def weights(n, dist, dtype):
+    r = ak.RngStream(seed=1)
+    return ak.gen_uniform(n, r, dtype=dtype) if dist == "uniform" else ak.gen_power_law(n, 1.0, r, dtype=dtype)
+
+
+def build_row(name, n, dist, dtype, out):
+    ws = weights(n, dist, dtype)
+    t = build_table(ws)
+    s = timed(lambda: build_table(ws, t))
+    bw = 4 if dtype == torch.float32 else 8
+    byts = n * (2 * bw + bw + 4)
+    rep = ak.validate_table(t, ws, tol=1e-4 if dtype == torch.float32 else 1e-6,
+                            row_tol=max(1e-9, 20 * n * 2.0**-53))
+    out.append(dict(config=name, op=f"psa_construct N={n:.0e} {dist} {str(dtype)[6:]}", seconds=s,
+                    rate=n / s, rate_unit="items/s", gbs=byts / s / 1e9, frac=byts / s / 1e9 / PEAK,
+                    parity=f"validate_table ok={rep.ok} worst={rep.worst_rel_error:.1e}"))
+    return ws, t
+
+
+def naive_row(name, t, m, out):
+    o = torch.empty(m, dtype=torch.int64, device="cuda")
+    for mode in ("philox4x32", "reference"):
+        s = timed(lambda: ak.sample_batch(t, m, ak.RngStream(1, 7), rng=mode, out=o), reps=3)
+        byts = m * (8 + (8 if t.dtype == torch.float32 else 16))
+        out.append(dict(config=name, op=f"sample_batch M={m:.0e} rng={mode}", seconds=s, rate=m / s,
+                        rate_unit="samples/s", gbs=byts / s / 1e9, frac=byts / s / 1e9 / PEAK,
+                        parity="bit-exact vs oracle: tests/test_gpu_sample.py"))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--json")
+    a = ap.parse_args()
+    out = []
+    ws, t = build_row("C1", 10**6, "uniform", torch.float64, out)
+    naive_row("C1", t, 10**6, out)
+    del ws, t
+    ws, t = build_row("C2", 10**8, "uniform", torch.float32, out)
+    naive_row("C2", t, 10**9, out)
+    del ws, t
+    for dt in (torch.float32, torch.float64):
+        ws, t = build_row("C3", 10**8, "zipf", dt, out)
+        del ws, t
+    ws, t = build_row("C5", 10**9, "uniform", torch.float32, out)
+    # C4: one sectioned pass of the bench
+    N, M, S = 10**9, 10**11, 1 << 14
+    asg = ak.assign_sections(N, S, M, 1, 7)
+    cd = torch.from_numpy(asg.counts).cuda()
+    od = torch.from_numpy(np.concatenate([[0], np.cumsum(asg.counts)[:-1]])).cuda()
+    k, tot = 0, 0
+    while k < asg.n_sections and tot + int(asg.counts[k]) <= (1 << 30):
+        tot += int(asg.counts[k])
+        k += 1
+    o = torch.empty(tot, dtype=torch.int64, device="cuda")
+    for mode in ("philox4x32", "reference"):
+        s = timed(lambda: sectioned_sample_into(t, S, cd, od, 0, k, ak.RngStream(1, 7), o, 0, mode), reps=3)
+        byts = tot * 8 + k * S * 8
+        out.append(dict(config="C4", op=f"sectioned pass {tot:.3e} draws / {k} sections rng={mode}",
+                        seconds=s, rate=tot / s, rate_unit="samples/s", gbs=byts / s / 1e9,
+                        frac=byts / s / 1e9 / PEAK, parity="bit-exact (reference rng) vs oracle: tests"))
+    del ws, t, o
+    ws, t = build_row("C5", 10**9, "uniform", torch.float64, out)
+    for r in out:
+        print(f"{r['config']:3s} {r['op']:55s} {r['seconds'] * 1e3:9.3f} ms  {r['rate']:.3e} {r['rate_unit']:9s} "
+              f"{r['gbs']:7.0f} GB/s  {100 * r['frac']:5.1f}%  {r['parity']}")
+    if a.json:
+        json.dump(dict(peak_gbs=PEAK, rows=out), open(a.json, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
