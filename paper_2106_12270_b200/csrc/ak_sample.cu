@@ -118,56 +118,6 @@ __global__ void k_rule_uniforms(const RowT *__restrict__ rows, double avg, i64 l
 // ---------------------------------------------------------------------------
 // sectioned sampler
 // ---------------------------------------------------------------------------
-// Philox2x64-10 with a precomputed key schedule (the per-round keys depend
-// on the seed only, so they are hoisted out of the draw loop).
-struct KeySched64 {
-    u64 k[10];
-};
-__device__ __forceinline__ KeySched64 sched64(u64 key)
-{
-    KeySched64 s;
-#pragma unroll
-    for (int r = 0; r < 10; ++r) s.k[r] = key + (u64)r * AK_PHILOX_WEYL;
-    return s;
-}
-__device__ __forceinline__ u64 philox64_sched(u64 x0, u64 x1, const KeySched64 &s)
-{
-#pragma unroll
-    for (int r = 0; r < 10; ++r) {
-        u64 hi = __umul64hi(x0, AK_PHILOX_MULT);
-        u64 lo = x0 * AK_PHILOX_MULT;
-        x0 = hi ^ s.k[r] ^ x1;
-        x1 = lo;
-    }
-    return x0;
-}
-struct KeySched32 {
-    uint2 k[10];
-};
-__device__ __forceinline__ KeySched32 sched32(u64 seed)
-{
-    KeySched32 s;
-    uint2 k = make_uint2((u32)seed, (u32)(seed >> 32));
-#pragma unroll
-    for (int r = 0; r < 10; ++r) {
-        s.k[r] = k;
-        k.x += AK_PH4_W0;
-        k.y += AK_PH4_W1;
-    }
-    return s;
-}
-__device__ __forceinline__ void philox32_sched(u64 call, u64 strm, const KeySched32 &s, u64 &a, u64 &b)
-{
-    uint4 c = make_uint4((u32)call, (u32)(call >> 32), (u32)strm, (u32)(strm >> 32));
-#pragma unroll
-    for (int r = 0; r < 10; ++r) {
-        u32 hi0 = __umulhi(AK_PH4_M0, c.x), lo0 = AK_PH4_M0 * c.x;
-        u32 hi1 = __umulhi(AK_PH4_M1, c.z), lo1 = AK_PH4_M1 * c.z;
-        c = make_uint4(hi1 ^ c.y ^ s.k[r].x, lo1, hi0 ^ c.w ^ s.k[r].y, lo0);
-    }
-    a = ((u64)c.y << 32) | c.x;
-    b = ((u64)c.w << 32) | c.z;
-}
 
 // The bucket rule from a raw 64-bit word.  For a power-of-two span 2^b the
 // reference's f64 steps x = u*span, k = trunc(x), x - k (span >= 2) are exact bit
