@@ -24,15 +24,16 @@
 // and compared with a local key.
 //
 // Pipeline (four kernels):
-//  1. k_build_scan   one pass over the weights (128-bit loads): classify, chunk
-//                    scans, per-tile totals and chunk bounds; a single-pass
-//                    decoupled look-back over super-tiles (32 tiles per CTA,
-//                    so the inclusive frontier outruns DRAM) produces the
-//                    exclusive tile bases DLb[t], DHb[t] (exact double-double
-//                    sums) and light counts kL[t].
+//  1. k_build_scan   one pass over the weights, streamed chunk by chunk
+//                    through a per-warp ring of shared-memory slots filled by
+//                    1-D bulk async copies (TMA): classify, per-chunk totals
+//                    (reduce-scatter), light counts, first heavies, the
+//                    light bitmask, the tile's monotone chunk bounds; a
+//                    single-pass decoupled look-back over super-tiles (32
+//                    tiles per CTA) produces the exclusive tile bases DLb[t],
+//                    DHb[t] (double-double sums) and light counts kL[t].
 //  2. k_build_coarse merge of the two tile-boundary sequences: for each tile
 //                    the first heavy tile covering its light keys (T1) and
-//                    the first light tile covering its heavy keys (S1), and
 //                    the first heavy after it (nextH).
 //  3. k_build_split  PSA split: for every section (light tile) boundary, the
 //                    heavy rank J = #heavies with key <= DLb[u] (tile from the
@@ -41,8 +42,11 @@
 //  4. k_build_pack   CTA per section: the tile's lights and the heavies of
 //                    ranks [J(u), J(u+1)) (any tiles; L2-resident, being the
 //                    lights' neighbours in key space) are merged once by a
-//                    merge path; each row is written exactly once.
-//  DRAM traffic ~ read w twice + write the rows once = the algorithmic bytes.
+//                    merge path over order-preserving 64-bit integer keys in
+//                    shared memory; each row is written exactly once (light
+//                    rows by consecutive threads, coalesced).
+//  DRAM traffic ~ read w twice + write the rows once = the algorithmic bytes
+//  (ncu: profiles/r1c_ncu_bench_pass.json).
 #include "ak_common.cuh"
 
 namespace {
@@ -203,26 +207,6 @@ __device__ __forceinline__ void lane_class(const double v[VV], double avg, doubl
     if (lane == 0) excl = 0.0;
     total = inc;  // unused by callers that take bounds from pass 1
     mask = m;
-}
-
-// Lane sums of one class and the canonical chunk total: a butterfly (xor)
-// tree sum, identical in every lane and every kernel.
-template <bool LIGHT>
-__device__ __forceinline__ double chunk_total(const double v[VV], double avg, u32 &mask)
-{
-    double s = 0.0;
-    u32 m = 0;
-#pragma unroll
-    for (int k = 0; k < VV; ++k) {
-        const bool valid = v[k] >= 0.0;
-        const bool in = LIGHT ? (valid && v[k] <= avg) : (valid && v[k] > avg);
-        if (in) s = s + (LIGHT ? (avg - v[k]) : (v[k] - avg));
-        m |= (u32)in << k;
-    }
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) s = s + __shfl_xor_sync(0xffffffffu, s, d);
-    mask = m;
-    return s;
 }
 
 // Canonical keys of one class given the chunk's [base, bound].
@@ -637,8 +621,6 @@ __device__ __forceinline__ dd add_dd_d(dd d, double x)
     fast_two_sum(s, e, h, l);
     return dd_make(h, l);
 }
-// X <= f for normalised X
-__device__ __forceinline__ bool le_dd_d(dd X, double f) { return X.hi < f || (X.hi == f && X.lo <= 0.0); }
 
 __device__ __forceinline__ u64 heavies_before_tile(const BuildWs &W, u64 n, u64 t)
 {
@@ -798,8 +780,6 @@ __device__ __forceinline__ void chunk_ranks(const BuildWs &W, u64 n, u64 g0, int
     const u64 base = (g0 < nch ? heavies_before_tile(W, n, t0) : heavies_before_tile(W, n, W.nt)) + pre;
     hb = g < nch ? base + (inc - hc) : ~0ull;
 }
-
-__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7FF0000000000000ll); }
 
 template <typename T>
 __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u64 n, double avg,
