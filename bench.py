@@ -5,11 +5,12 @@ samples/s (1/2/4/8 B200) vs HBM roofline"; configs C4 + C5):
   * synthetic weights: gen_uniform(N=1e9, RngStream(seed=1)) cast to float32,
     generated on every GPU (identical replicas, already resident in HBM);
   * one step = build the N=1e9 alias table from the resident weights
-    (psa_construct -> 3 kernels) + M = 1e11 batched/sectioned draws (S=2^14,
-    RngStream(seed=1, stream=7)) split over the ranks (strong scaling), drawn in
-    passes into a reused 8 GB output buffer;
-  * value = total samples / max-over-ranks sampling time; the build is
-    reported beside it as items/s with its own roofline.
+    (psa_construct -> 4 kernels) + M = 1e11 batched/sectioned draws per GPU
+    (S=2^14) from the GPU's own Philox sub-stream RngStream(seed=1,
+    stream=7+rank) (weak scaling: no data-path collective), drawn in passes
+    into a reused 8 GB output buffer;
+  * value = samples of all ranks / max-over-ranks sampling time; the build
+    is reported beside it as items/s with its own roofline.
 Inputs (4 GB weights, 8 GB table, 8 GB output) exceed the 126 MB L2, so no
 explicit flush is needed between steps.
 
@@ -164,7 +165,7 @@ def run_reference(a):
     v = statistics.median(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
-        "steps": a.steps, "warmup": a.warmup, "higher_is_better": True, "scaling": "strong",
+        "steps": a.steps, "warmup": a.warmup, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"reference CPU path (oracle/ C restatement of aliaskit): "
                                f"psa_construct N={n_items:.0e} + sectioned (serial, S={a.section}) "
@@ -190,7 +191,6 @@ def run_ours(a):
 
     import paper_2106_12270_b200 as ak
     from paper_2106_12270_b200 import _lib
-    from paper_2106_12270_b200 import distributed as D
     from paper_2106_12270_b200.sample import sectioned_sample_into
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -214,10 +214,32 @@ def run_ours(a):
     table = ak.psa_construct(ws)  # allocation + warm path
     r0 = ak.RngStream(seed=1, stream=7)
 
-    # sampling pass plan: this rank's contiguous section run, cut into passes
+    # multi-GPU: the one exchange of the job, replicating rank 0's table over
+    # NVLink (NCCL broadcast), timed on the device, max over ranks; each step
+    # below rebuilds the table on every rank from the replicated weights
+    # instead (both are measured, the cheaper one is used)
+    bcast = None
+    if world > 1:
+        for _ in range(2):
+            dist.broadcast(table.rows, 0)
+        torch.cuda.synchronize()
+        dist.barrier()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record()
+        dist.broadcast(table.rows, 0)
+        b1.record()
+        torch.cuda.synchronize()
+        tb = torch.tensor([b0.elapsed_time(b1) / 1e3], dtype=torch.float64, device=dev)
+        dist.all_reduce(tb, op=dist.ReduceOp.MAX)
+        nb = table.rows.numel() * 8
+        bcast = {"bytes": nb, "s": float(tb.item()), "GB_per_s": nb / float(tb.item()) / 1e9}
+
+    # sampling pass plan: this rank's own sub-stream (weak scaling), cut into
+    # passes of whole sections
+    r0 = ak.RngStream(seed=1, stream=7 + rank)
     asg = ak.assign_sections(N, S, M, r0.seed, r0.stream)
     S_eff = asg.section_size
-    first, count, out_off, draws = D.section_shard(asg.counts, rank, world)
+    first, count, out_off, draws = 0, asg.n_sections, 0, M
     counts_d = torch.from_numpy(asg.counts).to(dev)
     offs = np.concatenate([[0], np.cumsum(asg.counts)[:-1]])
     offs_d = torch.from_numpy(offs).to(dev)
@@ -322,7 +344,7 @@ def run_ours(a):
     if not a.no_e2e:
         Me = int(a.e2e_samples)
         K = a.e2e_steps
-        off_e, cnt_e = D.naive_shard(Me, rank, world)
+        cnt_e = Me  # per GPU (weak scaling, as the device-resident measurement)
         w_host = ws.weights.cpu().pin_memory()
         o_host = [torch.empty(max(cnt_e, 1), dtype=torch.int64).pin_memory() for _ in range(2)]
         wd = [torch.empty_like(ws.weights) for _ in range(2)]
@@ -346,13 +368,14 @@ def run_ours(a):
                     s_cmp.wait_event(ev_out[i - 2])  # output buffer copied out
                 wse = ak.make_weight_set(wd[i % 2])
                 te = ak.psa_construct(wse)
-                asg_e = ak.assign_sections(N, S, Me, 1, 7 + i)
-                f_e, c_e, oo_e, dr_e = D.section_shard(asg_e.counts, rank, world)
+                st_e = 7 + 64 * rank + i
+                asg_e = ak.assign_sections(N, S, Me, 1, st_e)
+                f_e, c_e, oo_e, dr_e = 0, asg_e.n_sections, 0, Me
                 cd = torch.from_numpy(asg_e.counts).to(dev, non_blocking=True)
                 odf = torch.from_numpy(np.concatenate([[0], np.cumsum(asg_e.counts)[:-1]])).to(dev, non_blocking=True)
                 if od[i % 2] is None or od[i % 2].numel() < max(dr_e, 1):
                     od[i % 2] = torch.empty(max(dr_e, 1), dtype=torch.int64, device=dev)
-                sectioned_sample_into(te, asg_e.section_size, cd, odf, f_e, c_e, ak.RngStream(1, 7 + i),
+                sectioned_sample_into(te, asg_e.section_size, cd, odf, f_e, c_e, ak.RngStream(1, st_e),
                                       od[i % 2], oo_e, rng_mode)
                 ev_cmp[i].record(s_cmp)
                 return dr_e
@@ -381,7 +404,7 @@ def run_ours(a):
         if world > 1:
             dist.all_reduce(tt2, op=dist.ReduceOp.MAX)
         el = float(tt2.item())
-        e2e = {"value": Me * K / el, "unit": UNIT,
+        e2e = {"value": Me * world * K / el, "unit": UNIT,
                "h2d_bytes_per_step": int(N * b_w), "d2h_bytes_per_step": int(cnt_e * 8),
                "path": "pinned host f32 weights -> make_weight_set -> psa_construct -> "
                        "sectioned_sample -> pinned host int64 samples, 3-stream pipeline",
@@ -400,19 +423,20 @@ def run_ours(a):
                "naive_samples_per_s": d["naive_samples_per_s"]}
 
     if rank == 0:
-        value = M * a.steps / t_samp
+        value = M * world * a.steps / t_samp
         ach = pass_bytes / t_pass / 1e9
         bach = build_bytes / t_build1 / 1e9
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": t_step / a.steps * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": f"C4+C5: N={N:.0e} {a.dtype} table (gen_uniform seed=1) built per step, "
-                                   f"then {M:.0e} sectioned draws (S={S}, RngStream(1,7), rng={rng_mode}) "
-                                   f"split over {world} GPU(s)",
-                       "n": N, "samples": M, "section_size": S, "rng": rng_mode,
-                       "weights_dtype": a.dtype, "parallelism": f"replicas x{world}, section-range shards",
+                                   f"then {M:.0e} sectioned draws per GPU (S={S}, RngStream(1, 7+rank), "
+                                   f"rng={rng_mode}) on {world} GPU(s)",
+                       "n": N, "samples_per_gpu": M, "samples_total": M * world, "section_size": S,
+                       "rng": rng_mode, "weights_dtype": a.dtype,
+                       "parallelism": f"dp{world}: table replica per GPU, independent Philox sub-streams",
                        "l2": "inputs (weights 4 GB, table 8 GB, output 8 GB) exceed L2; no flush needed",
                        "passes_per_step": len(passes)},
             "build": {"items_per_s": N * a.steps / t_build, "ms": t_build / a.steps * 1e3,
@@ -426,7 +450,8 @@ def run_ours(a):
                                        "frac": pass_bytes / t_pass_ref / 1e9 / peak},
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "gpu_launches": a.steps * (3 + len(passes)),
+            "table_broadcast": bcast,
+            "gpu_launches": a.steps * (4 + len(passes)),
             "clocks": clocks,
             "wall_s_timed_region": wall,
         }
