@@ -125,7 +125,7 @@ __global__ void k_rule_uniforms(const RowT *__restrict__ rows, double avg, i64 l
 // scaled by 2^(b-53) (built as 1.f - 1.0, exact) — bit-identical results
 // with four fewer double operations.  Other spans use the f64 rule.
 template <typename RowT>
-__device__ __forceinline__ i64 rule_word(const RowT *tab, u64 word, i64 span, int b, bool pow2,
+__device__ __forceinline__ i64 rule_word(const RowT &tab, u64 word, i64 span, int b, bool pow2,
                                          i64 lo, double avg)
 {
     i64 k;
@@ -140,9 +140,23 @@ __device__ __forceinline__ i64 rule_word(const RowT *tab, u64 word, i64 span, in
         if (k >= span) k = span - 1;
         frac = x - (double)k;
     }
-    const RowT r = tab[k];
+    const auto r = tab[k];
     return (frac * avg < (double)r.tw) ? (lo + k + 1) : (i64)r.alias;
 }
+
+// A staged f64 section laid out as separate threshold / alias arrays (12
+// bytes per row), so 2^14-row sections of f64 tables fit in shared memory.
+struct SoA64View {
+    const double *tw;
+    const u32 *al;
+    __device__ __forceinline__ RowF64 operator[](i64 k) const
+    {
+        RowF64 r;
+        r.tw = tw[k];
+        r.alias = al[k];
+        return r;
+    }
+};
 
 // Draw pair (d0, d1) of output slots (o0, o0 + 1) written with 16-byte
 // stores where possible.  `par` = 1 when o0 is not 16-byte aligned: then
@@ -257,7 +271,7 @@ __device__ __forceinline__ void fast_pairs_f32(const RowF32 *tab, u32 cl0, u32 c
 // consecutive draws per step (one Philox4x32-10 call in the fast mode) and
 // the warp writes them as 16-byte stores.  STAGE=false reads rows from
 // global memory (sections too large for shared memory).
-template <typename RowT, int MODE, bool STAGE>
+template <typename RowT, int MODE, int SMODE>
 __global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
     const RowT *__restrict__ rows, u64 n, double avg, u64 S, const i64 *__restrict__ counts,
     const i64 *__restrict__ offsets, u64 first, u64 count, u64 seed, u64 stream_id, u64 ctr0,
@@ -265,10 +279,15 @@ __global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) u64 bar;
+    // SMODE 0: rows read from global memory; 1: raw rows staged by a bulk
+    // async copy; 2: f64 rows staged as threshold / alias arrays
+    constexpr bool STAGE = SMODE != 0;
     RowT *srows = reinterpret_cast<RowT *>(smem_raw);
+    double *stw = reinterpret_cast<double *>(smem_raw);
+    u32 *sal = reinterpret_cast<u32 *>(stw + S);
     const int lane = threadIdx.x & 31;
     u32 phase = 0;
-    if (STAGE && threadIdx.x == 0) {
+    if (SMODE == 1 && threadIdx.x == 0) {
         mbar_init(&bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -303,7 +322,7 @@ __global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
         const bool pow2 = span >= 2 && (span & (span - 1)) == 0;
         const int bb = pow2 ? __ffsll(span) - 1 : 0;
         const RowT *src = rows + lo;
-        if (STAGE) {
+        if (SMODE == 1) {
             // the previous section's rows are no longer read (generic proxy)
             // before the async-proxy copy overwrites them
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -320,8 +339,16 @@ __global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
                 for (i64 r = threadIdx.x; r < span; r += blockDim.x) srows[r] = src[r];
                 __syncthreads();
             }
+        } else if (SMODE == 2) {
+            __syncthreads();
+            for (i64 r = threadIdx.x; r < span; r += blockDim.x) {
+                const RowF64 x = ld_row(reinterpret_cast<const RowF64 *>(src) + r);
+                stw[r] = x.tw;
+                sal[r] = (u32)x.alias;
+            }
+            __syncthreads();
         }
-        const RowT *tab = STAGE ? srows : src;
+        const RowT *tabp = SMODE == 1 ? srows : src;
         const u64 strm = ak_derive(seed, stream_id, j, AK_SALT_SECTION);
         i64 *o = out + (oj - out_base);
         // pairs: pair p holds draws (2p - poff, 2p - poff + 1).  The fast RNG
@@ -332,7 +359,7 @@ __global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
         const int par = MODE == AK_RNG_REFERENCE ? 0 : (int)((obit + (int)poff) & 1);
         const i64 p0 = (ia + poff) >> 1, p1 = (ib - 1 + poff) >> 1;  // inclusive
         // checked pairs [ps, pe] (every lane of the CTA iterates together)
-        auto generic = [&](i64 ps, i64 pe) {
+        auto generic_on = [&](const auto &tab, i64 ps, i64 pe) {
             for (i64 pb = ps; pb <= pe; pb += blockDim.x) {
                 const i64 p = pb + threadIdx.x;
                 const i64 i0 = 2 * p - poff;
@@ -355,7 +382,11 @@ __global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
                 store_pair(o + i0, d0, d1, v0, v1, par, lane);
             }
         };
-        if (MODE == AK_RNG_PHILOX4X32 && sizeof(RowT) == 8 && STAGE && pow2) {
+        auto generic = [&](i64 ps, i64 pe) {
+            if constexpr (SMODE == 2) generic_on(SoA64View{stw, sal}, ps, pe);
+            else generic_on(tabp, ps, pe);
+        };
+        if (MODE == AK_RNG_PHILOX4X32 && sizeof(RowT) == 8 && SMODE == 1 && pow2) {
             // interior pairs q = p - p0 in [qa, qa + nfast): both draws in
             // range, the call counter's high word constant, whole CTA steps
             const i64 np = p1 - p0 + 1;
@@ -366,7 +397,7 @@ __global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
             if ((u64)(u32)cb + (u64)(qa + nfast) > 0xFFFFFFFFull) nfast = 0;
             if (nfast > 0) {
                 if (qa > 0) generic(p0, p0 + qa - 1);
-                fast_pairs_f32(reinterpret_cast<const RowF32 *>(tab), (u32)cb, (u32)(cb >> 32),
+                fast_pairs_f32(reinterpret_cast<const RowF32 *>(tabp), (u32)cb, (u32)(cb >> 32),
                                strm, seed, o + (2 * p0 - poff), (u32)qa, (u32)(qa + nfast), bb,
                                (u32)(lo + 1), avg, par, lane);
                 if (qa + nfast < np) generic(p0 + qa + nfast, p1);
@@ -401,15 +432,15 @@ int launch_naive(const void *rows, double avg, u64 lo, u64 span, u64 seed, u64 s
     return AK_OK;
 }
 
-template <typename RowT, int MODE, bool STAGE>
+template <typename RowT, int MODE, int SMODE>
 int launch_sectioned_t(const void *rows, u64 n, double avg, u64 S, const i64 *counts,
                        const i64 *offsets, u64 first, u64 count, u64 seed, u64 sid, u64 ctr0,
                        i64 *out, i64 out_base, cudaStream_t st)
 {
-    size_t smem = STAGE ? S * sizeof(RowT) : 0;
-    auto kern = k_sample_sectioned<RowT, MODE, STAGE>;
-    if (STAGE) AK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = STAGE ? (smem > 110 * 1024 ? 1 : 2) : 2;
+    size_t smem = SMODE == 1 ? S * sizeof(RowT) : (SMODE == 2 ? S * 12 : 0);
+    auto kern = k_sample_sectioned<RowT, MODE, SMODE>;
+    if (SMODE) AK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = SMODE ? (smem > 110 * 1024 ? 1 : 2) : 2;
     u64 g = (u64)ak_num_sms() * per_sm;
     kern<<<(unsigned)g, 1024, smem, st>>>((const RowT *)rows, n, avg, S, counts, offsets, first,
                                           count, seed, sid, ctr0, out, out_base);
@@ -417,28 +448,31 @@ int launch_sectioned_t(const void *rows, u64 n, double avg, u64 S, const i64 *co
     return AK_OK;
 }
 
+template <typename RowT, int MODE>
+int launch_sectioned_m(const void *rows, u64 n, double avg, u64 S, const i64 *counts,
+                       const i64 *offsets, u64 first, u64 count, u64 seed, u64 sid, u64 ctr0,
+                       i64 *out, i64 out_base, cudaStream_t st)
+{
+    if (S * sizeof(RowT) <= 200 * 1024)
+        return launch_sectioned_t<RowT, MODE, 1>(rows, n, avg, S, counts, offsets, first, count,
+                                                 seed, sid, ctr0, out, out_base, st);
+    if (sizeof(RowT) == 16 && S * 12 <= 200 * 1024 && n < 0xFFFFFFFFull)
+        return launch_sectioned_t<RowT, MODE, 2>(rows, n, avg, S, counts, offsets, first, count,
+                                                 seed, sid, ctr0, out, out_base, st);
+    return launch_sectioned_t<RowT, MODE, 0>(rows, n, avg, S, counts, offsets, first, count, seed,
+                                             sid, ctr0, out, out_base, st);
+}
+
 template <typename RowT>
 int launch_sectioned(const void *rows, u64 n, double avg, u64 S, const i64 *counts,
                      const i64 *offsets, u64 first, u64 count, u64 seed, u64 sid, u64 ctr0,
                      i64 *out, i64 out_base, int mode, cudaStream_t st)
 {
-    const bool stage = S * sizeof(RowT) <= 200 * 1024;
-    if (mode == AK_RNG_REFERENCE) {
-        if (stage)
-            return launch_sectioned_t<RowT, AK_RNG_REFERENCE, true>(rows, n, avg, S, counts, offsets,
-                                                                    first, count, seed, sid, ctr0,
-                                                                    out, out_base, st);
-        return launch_sectioned_t<RowT, AK_RNG_REFERENCE, false>(rows, n, avg, S, counts, offsets,
-                                                                 first, count, seed, sid, ctr0,
-                                                                 out, out_base, st);
-    }
-    if (stage)
-        return launch_sectioned_t<RowT, AK_RNG_PHILOX4X32, true>(rows, n, avg, S, counts, offsets,
-                                                                 first, count, seed, sid, ctr0,
-                                                                 out, out_base, st);
-    return launch_sectioned_t<RowT, AK_RNG_PHILOX4X32, false>(rows, n, avg, S, counts, offsets,
-                                                              first, count, seed, sid, ctr0, out,
-                                                              out_base, st);
+    if (mode == AK_RNG_REFERENCE)
+        return launch_sectioned_m<RowT, AK_RNG_REFERENCE>(rows, n, avg, S, counts, offsets, first,
+                                                          count, seed, sid, ctr0, out, out_base, st);
+    return launch_sectioned_m<RowT, AK_RNG_PHILOX4X32>(rows, n, avg, S, counts, offsets, first,
+                                                       count, seed, sid, ctr0, out, out_base, st);
 }
 
 }  // namespace
