@@ -52,8 +52,8 @@ def parse():
     ap.add_argument("--dtype", default="float32", choices=["float32", "float64"])
     ap.add_argument("--e2e-samples", type=float, default=5e8)
     ap.add_argument("--e2e-steps", type=int, default=4)
-    ap.add_argument("--cpu-n", type=float, default=1e7)
-    ap.add_argument("--cpu-samples", type=float, default=5e7)
+    ap.add_argument("--cpu-n", type=float, default=1e8)
+    ap.add_argument("--cpu-samples", type=float, default=2e8)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
