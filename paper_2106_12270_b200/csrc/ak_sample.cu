@@ -15,9 +15,6 @@
 // by the chi-square tests, not bit-compatible with the reference).
 #include "ak_common.cuh"
 
-#ifndef AK_FAST_ILP2
-#define AK_FAST_ILP2 0
-#endif
 
 namespace {
 
@@ -232,8 +229,7 @@ __device__ __forceinline__ void store_pair_fast(i64 *p, u32 d0, u32 d1, int par,
 // draw in range.  Pair q is one Philox4x32-10 call (counter low word
 // cl0 + q, high word ch), its two 64-bit words are draws 2q and 2q + 1 of
 // ob.  Indices fit 32 bits (u32 aliases); outputs are written as int64 with
-// 16-byte stores (see store_pair for the misaligned case).  Two calls are
-// interleaved per thread for instruction-level parallelism.
+// 16-byte stores (see store_pair for the misaligned case).
 __device__ __forceinline__ void fast_pairs_f32(const RowF32 *tab, u32 cl0, u32 ch, u64 strm,
                                                u64 seed, i64 *ob, u32 qa, u32 qb,
                                                int b, u32 lo1, double avg, int par, int lane)
@@ -244,17 +240,6 @@ __device__ __forceinline__ void fast_pairs_f32(const RowF32 *tab, u32 cl0, u32 c
     const u64 fmask = (1ull << (53 - b)) - 1;
     const u32 step = blockDim.x;
     u32 q = qa + threadIdx.x;
-#if AK_FAST_ILP2
-    // (qb - qa) is a multiple of blockDim: every thread runs the same trips
-    for (; q + step < qb; q += 2 * step) {
-        const uint4 c0 = philox4x32_key(make_uint4(cl0 + q, ch, sl, sh), k0, k1);
-        const uint4 c1 = philox4x32_key(make_uint4(cl0 + q + step, ch, sl, sh), k0, k1);
-        store_pair_fast(ob + 2 * (u64)q, rule_f32_pow2(tab, c0.x, c0.y, sk, b, fmask, lo1, avg),
-                        rule_f32_pow2(tab, c0.z, c0.w, sk, b, fmask, lo1, avg), par, lane);
-        store_pair_fast(ob + 2 * (u64)(q + step), rule_f32_pow2(tab, c1.x, c1.y, sk, b, fmask, lo1, avg),
-                        rule_f32_pow2(tab, c1.z, c1.w, sk, b, fmask, lo1, avg), par, lane);
-    }
-#endif
     for (; q < qb; q += step) {
         const uint4 c0 = philox4x32_key(make_uint4(cl0 + q, ch, sl, sh), k0, k1);
         store_pair_fast(ob + 2 * (u64)q, rule_f32_pow2(tab, c0.x, c0.y, sk, b, fmask, lo1, avg),
