@@ -1,0 +1,43 @@
+"""bench.py keeps the driver contract: one JSON line with the required keys.
+The reference arm runs on the CPU (oracle port); our arm needs a GPU."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "higher_is_better", "scaling",
+        "vs_baseline", "dtype", "data", "config", "e2e", "cpu_baseline"}
+
+
+def run(args, timeout):
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args, capture_output=True,
+                       text=True, timeout=timeout, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_reference_arm_contract():
+    d = run(["--impl", "reference", "--steps", "1", "--warmup", "0", "--cpu-n", "1e5",
+             "--cpu-samples", "1e5"], 300)
+    assert KEYS <= set(d) and d["impl"] == "reference"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "port"
+    assert d["value"] > 0 and d["higher_is_better"] is True
+
+
+@pytest.mark.gpu
+def test_our_arm_contract():
+    d = run(["--steps", "1", "--warmup", "1", "--n", "1e6", "--samples", "1e8", "--no-cpu",
+             "--e2e-samples", "1e7", "--e2e-steps", "1"], 600)
+    assert KEYS <= set(d)
+    for k in ("roofline", "clocks", "gpu_launches", "build"):
+        assert k in d
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] > 0 and d["scaling"] == "weak"
