@@ -21,11 +21,17 @@ from .model import AliasTable, WeightSet
 from .partition import LightHeavyPartition, PrepackResult
 
 
+MAX_BLOCK = 11000  # 20 bytes of shared memory per item of a block (ak_prepack.cu)
+
+
 def _prepack(w: WeightSet, block_size: int, threshold: int):
     if block_size < 2:
         raise ValueError("block_size must be at least 2")
     if threshold < 1:
         raise ValueError("min_pair_threshold must be at least 1")
+    if block_size > MAX_BLOCK:
+        # a block's lights, heavies and keys live in one CTA's shared memory
+        raise ValueError(f"block_size {block_size} exceeds the device limit {MAX_BLOCK}")
     dev = w.weights.device
     n = w.n
     L = _lib.lib()
