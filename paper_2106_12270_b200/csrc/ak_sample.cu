@@ -181,12 +181,6 @@ __device__ __forceinline__ void store_pair(i64 *o0, i64 d0, i64 d1, bool v0, boo
     if (v0 && !prev_vec) o0[0] = d0;
 }
 
-// Fast-mode interior of a section (f32 rows staged in shared memory, span
-// 2^b): pairs q in [qa, qb) with qb - qa a multiple of the CTA size, every
-// draw in range.  Pair q is one Philox4x32-10 call (counter low word
-// cl0 + q, high word ch), its two 64-bit words are draws 2q and 2q + 1 of
-// ob.  Indices fit 32 bits (u32 aliases); outputs are written as int64 with
-// 16-byte stores (see store_pair for the misaligned case).
 // Philox4x32-10 with the round keys formed from the (warp-uniform) seed
 // words inline, so they live in uniform registers rather than per thread.
 __device__ __forceinline__ uint4 philox4x32_key(uint4 c, u32 k0, u32 k1)
@@ -200,51 +194,105 @@ __device__ __forceinline__ uint4 philox4x32_key(uint4 c, u32 k0, u32 k1)
     return c;
 }
 
+// Philox4x32-10 round keys (k0 + r W0, k1 + r W1), precomputed on the host
+// and passed by value: they sit in the kernel's constant bank and are used
+// as direct operands of the round XORs, so they take no registers.
+struct Ph4Keys {
+    u32 k[20];
+};
+
+Ph4Keys ph4_keys(u64 seed)
+{
+    Ph4Keys rk;
+    for (int r = 0; r < 10; ++r) {
+        rk.k[2 * r] = (u32)seed + (u32)r * AK_PH4_W0;
+        rk.k[2 * r + 1] = (u32)(seed >> 32) + (u32)r * AK_PH4_W1;
+    }
+    return rk;
+}
+
+__device__ __forceinline__ uint4 philox4x32_rk(uint4 c, const Ph4Keys &rk)
+{
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const u32 hi0 = __umulhi(AK_PH4_M0, c.x), lo0 = AK_PH4_M0 * c.x;
+        const u32 hi1 = __umulhi(AK_PH4_M1, c.z), lo1 = AK_PH4_M1 * c.z;
+        c = make_uint4(hi1 ^ c.y ^ rk.k[2 * r], lo1, hi0 ^ c.w ^ rk.k[2 * r + 1], lo0);
+    }
+    return c;
+}
+
 // the bucket rule for one 64-bit word on a staged f32 section of span 2^b
 __device__ __forceinline__ u32 rule_f32_pow2(const RowF32 *tab, u32 wl, u32 wh, int sk, int b,
                                              u64 fmask, u32 lo1, double avg)
 {
-    const u64 word = ((u64)wh << 32) | wl;
+    // the 53-b fraction bits (word bits 11 .. 63-b) as the mantissa of a
+    // double in [1, 2): ((word & ~0x7ff) << b) >> 12, in 32-bit halves
     const u32 k = wh >> sk;
-    const u64 f = (word >> 11) & fmask;
-    const double frac = __longlong_as_double((long long)(0x3FF0000000000000ull | (f << (b - 1)))) - 1.0;
+    const u32 l = wl & ~0x7FFu;
+    const u32 vh = __funnelshift_l(l, wh, b), vl = l << b;
+    const double frac = __hiloint2double((int)((vh >> 12) + 0x3FF00000u), (int)__funnelshift_r(vl, vh, 12)) - 1.0;
     const uint2 row = *reinterpret_cast<const uint2 *>(tab + k);
     return (frac * avg < (double)__uint_as_float(row.x)) ? lo1 + k : row.y;
-}
-
-__device__ __forceinline__ void store_pair_fast(i64 *p, u32 d0, u32 d1, int par, int lane)
-{
-    if (par == 0) {
-        *reinterpret_cast<longlong2 *>(p) = make_longlong2((long long)d0, (long long)d1);
-    } else {
-        const u32 nx = __shfl_down_sync(0xffffffffu, d0, 1);
-        if (lane < 31) *reinterpret_cast<longlong2 *>(p + 1) = make_longlong2((long long)d1, (long long)nx);
-        else p[1] = (i64)d1;
-        if (lane == 0) p[0] = (i64)d0;
-    }
 }
 
 // Fast-mode interior of a section (f32 rows staged in shared memory, span
 // 2^b): pairs q in [qa, qb) with qb - qa a multiple of the CTA size, every
 // draw in range.  Pair q is one Philox4x32-10 call (counter low word
 // cl0 + q, high word ch), its two 64-bit words are draws 2q and 2q + 1 of
-// ob.  Indices fit 32 bits (u32 aliases); outputs are written as int64 with
-// 16-byte stores (see store_pair for the misaligned case).
-__device__ __forceinline__ void fast_pairs_f32(const RowF32 *tab, u32 cl0, u32 ch, u64 strm,
-                                               u64 seed, i64 *ob, u32 qa, u32 qb,
-                                               int b, u32 lo1, double avg, int par, int lane)
+// ob.  Indices fit 32 bits (u32 aliases); outputs are int64.  PAR = 0: ob
+// is 16-byte aligned and each pair is one 16-byte store; PAR = 1: two 8-byte
+// stores (twice the store requests, but no shuffle or lane branch, which
+// cost 14% on the half of the sections whose output is misaligned).  The
+// store-request count matters: all-8-byte stores back up the LSU queue and
+// lose 30% (profiles/r1_summary.md).
+template <int PAR>
+__device__ __forceinline__ void store_fast(i64 *p, u32 d0, u32 d1, int lane)
+{
+    if (PAR == 0) {
+        *reinterpret_cast<uint4 *>(p) = make_uint4(d0, 0u, d1, 0u);
+    } else {
+        *reinterpret_cast<uint2 *>(p) = make_uint2(d0, 0u);
+        *reinterpret_cast<uint2 *>(p + 1) = make_uint2(d1, 0u);
+    }
+}
+
+template <int PAR, int U = 3>
+__device__ __forceinline__ void fast_pairs_f32_p(const RowF32 *tab, u32 cl0, u32 ch, u64 strm,
+                                                 const Ph4Keys &rk, i64 *ob, u32 qa, u32 qb, int b,
+                                                 u32 lo1, double avg, int lane)
 {
     const u32 sl = (u32)strm, sh = (u32)(strm >> 32);
-    const u32 k0 = (u32)seed, k1 = (u32)(seed >> 32);
     const int sk = 32 - b;
     const u64 fmask = (1ull << (53 - b)) - 1;
     const u32 step = blockDim.x;
+    i64 *p = ob + 2 * (u64)(qa + threadIdx.x);
     u32 q = qa + threadIdx.x;
-    for (; q < qb; q += step) {
-        const uint4 c0 = philox4x32_key(make_uint4(cl0 + q, ch, sl, sh), k0, k1);
-        store_pair_fast(ob + 2 * (u64)q, rule_f32_pow2(tab, c0.x, c0.y, sk, b, fmask, lo1, avg),
-                        rule_f32_pow2(tab, c0.z, c0.w, sk, b, fmask, lo1, avg), par, lane);
+    // U independent calls in flight per thread: the rounds are a serial
+    // multiply-xor chain and 32 warps per SM alone leave it latency bound
+    // (U = 1 -> 2: +5%, 3: +1% more, 4 slower; tools/time_sectioned.py).
+    for (; q + (U - 1) * step < qb; q += U * step, p += 2 * U * (u64)step) {
+        uint4 c[U];
+#pragma unroll
+        for (int z = 0; z < U; ++z) c[z] = philox4x32_rk(make_uint4(cl0 + q + z * step, ch, sl, sh), rk);
+#pragma unroll
+        for (int z = 0; z < U; ++z)
+            store_fast<PAR>(p + 2 * z * (u64)step, rule_f32_pow2(tab, c[z].x, c[z].y, sk, b, fmask, lo1, avg),
+                            rule_f32_pow2(tab, c[z].z, c[z].w, sk, b, fmask, lo1, avg), lane);
     }
+    for (; q < qb; q += step, p += 2 * (u64)step) {
+        const uint4 c0 = philox4x32_rk(make_uint4(cl0 + q, ch, sl, sh), rk);
+        store_fast<PAR>(p, rule_f32_pow2(tab, c0.x, c0.y, sk, b, fmask, lo1, avg),
+                        rule_f32_pow2(tab, c0.z, c0.w, sk, b, fmask, lo1, avg), lane);
+    }
+}
+
+__device__ __forceinline__ void fast_pairs_f32(const RowF32 *tab, u32 cl0, u32 ch, u64 strm,
+                                               const Ph4Keys &rk, i64 *ob, u32 qa, u32 qb,
+                                               int b, u32 lo1, double avg, int par, int lane)
+{
+    if (par) fast_pairs_f32_p<1>(tab, cl0, ch, strm, rk, ob, qa, qb, b, lo1, avg, lane);
+    else fast_pairs_f32_p<0>(tab, cl0, ch, strm, rk, ob, qa, qb, b, lo1, avg, lane);
 }
 
 // Sectioned sampling.  The draws of sections [first, first+count) form one
@@ -254,13 +302,13 @@ __device__ __forceinline__ void fast_pairs_f32(const RowF32 *tab, u32 cl0, u32 c
 // stages each section's rows in shared memory once (cp.async.bulk +
 // mbarrier) and serves every draw from there.  Each thread produces two
 // consecutive draws per step (one Philox4x32-10 call in the fast mode) and
-// the warp writes them as 16-byte stores.  STAGE=false reads rows from
+// the warp writes them as 16-byte stores where aligned.  SMODE 0 reads rows from
 // global memory (sections too large for shared memory).
 template <typename RowT, int MODE, int SMODE>
 __global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
     const RowT *__restrict__ rows, u64 n, double avg, u64 S, const i64 *__restrict__ counts,
     const i64 *__restrict__ offsets, u64 first, u64 count, u64 seed, u64 stream_id, u64 ctr0,
-    i64 *__restrict__ out, i64 out_base)
+    i64 *__restrict__ out, i64 out_base, const Ph4Keys rk)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) u64 bar;
@@ -383,7 +431,7 @@ __global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
             if (nfast > 0) {
                 if (qa > 0) generic(p0, p0 + qa - 1);
                 fast_pairs_f32(reinterpret_cast<const RowF32 *>(tabp), (u32)cb, (u32)(cb >> 32),
-                               strm, seed, o + (2 * p0 - poff), (u32)qa, (u32)(qa + nfast), bb,
+                               strm, rk, o + (2 * p0 - poff), (u32)qa, (u32)(qa + nfast), bb,
                                (u32)(lo + 1), avg, par, lane);
                 if (qa + nfast < np) generic(p0 + qa + nfast, p1);
                 continue;
@@ -428,7 +476,7 @@ int launch_sectioned_t(const void *rows, u64 n, double avg, u64 S, const i64 *co
     int per_sm = SMODE ? (smem > 110 * 1024 ? 1 : 2) : 2;
     u64 g = (u64)ak_num_sms() * per_sm;
     kern<<<(unsigned)g, 1024, smem, st>>>((const RowT *)rows, n, avg, S, counts, offsets, first,
-                                          count, seed, sid, ctr0, out, out_base);
+                                          count, seed, sid, ctr0, out, out_base, ph4_keys(seed));
     AK_LAUNCH_CHECK("k_sample_sectioned");
     return AK_OK;
 }
