@@ -295,6 +295,47 @@ __device__ __forceinline__ void fast_pairs_f32(const RowF32 *tab, u32 cl0, u32 c
     else fast_pairs_f32_p<0>(tab, cl0, ch, strm, rk, ob, qa, qb, b, lo1, avg, lane);
 }
 
+// The same interior loop for f64 tables staged in shared memory, either as
+// rows (V = const RowF64 *) or as threshold / alias arrays (V = SoA64View);
+// indices fit 32 bits (n < 2^32 is checked by the caller).
+template <class V>
+__device__ __forceinline__ u32 rule_f64_pow2(const V &tab, u32 wl, u32 wh, int sk, int b, u32 lo1,
+                                             double avg)
+{
+    const u32 k = wh >> sk;
+    const u32 l = wl & ~0x7FFu;
+    const u32 vh = __funnelshift_l(l, wh, b), vl = l << b;
+    const double frac = __hiloint2double((int)((vh >> 12) + 0x3FF00000u), (int)__funnelshift_r(vl, vh, 12)) - 1.0;
+    const RowF64 row = tab[k];
+    return (frac * avg < row.tw) ? lo1 + k : (u32)row.alias;
+}
+
+template <class V, int PAR, int U = 3>
+__device__ __forceinline__ void fast_pairs_f64_p(const V &tab, u32 cl0, u32 ch, u64 strm,
+                                                 const Ph4Keys &rk, i64 *ob, u32 qa, u32 qb, int b,
+                                                 u32 lo1, double avg, int lane)
+{
+    const u32 sl = (u32)strm, sh = (u32)(strm >> 32);
+    const int sk = 32 - b;
+    const u32 step = blockDim.x;
+    i64 *p = ob + 2 * (u64)(qa + threadIdx.x);
+    u32 q = qa + threadIdx.x;
+    for (; q + (U - 1) * step < qb; q += U * step, p += 2 * U * (u64)step) {
+        uint4 c[U];
+#pragma unroll
+        for (int z = 0; z < U; ++z) c[z] = philox4x32_rk(make_uint4(cl0 + q + z * step, ch, sl, sh), rk);
+#pragma unroll
+        for (int z = 0; z < U; ++z)
+            store_fast<PAR>(p + 2 * z * (u64)step, rule_f64_pow2(tab, c[z].x, c[z].y, sk, b, lo1, avg),
+                            rule_f64_pow2(tab, c[z].z, c[z].w, sk, b, lo1, avg), lane);
+    }
+    for (; q < qb; q += step, p += 2 * (u64)step) {
+        const uint4 c0 = philox4x32_rk(make_uint4(cl0 + q, ch, sl, sh), rk);
+        store_fast<PAR>(p, rule_f64_pow2(tab, c0.x, c0.y, sk, b, lo1, avg),
+                        rule_f64_pow2(tab, c0.z, c0.w, sk, b, lo1, avg), lane);
+    }
+}
+
 // Sectioned sampling.  The draws of sections [first, first+count) form one
 // section-major index space (offsets = exclusive prefix of counts); CTA b
 // takes the contiguous slice [D*b/G, D*(b+1)/G) of it, so every CTA does the
@@ -419,7 +460,7 @@ __global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
             if constexpr (SMODE == 2) generic_on(SoA64View{stw, sal}, ps, pe);
             else generic_on(tabp, ps, pe);
         };
-        if (MODE == AK_RNG_PHILOX4X32 && sizeof(RowT) == 8 && SMODE == 1 && pow2) {
+        if (MODE == AK_RNG_PHILOX4X32 && SMODE != 0 && pow2 && (sizeof(RowT) == 8 || n <= 0xFFFFFFFFull)) {
             // interior pairs q = p - p0 in [qa, qa + nfast): both draws in
             // range, the call counter's high word constant, whole CTA steps
             const i64 np = p1 - p0 + 1;
@@ -430,9 +471,20 @@ __global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
             if ((u64)(u32)cb + (u64)(qa + nfast) > 0xFFFFFFFFull) nfast = 0;
             if (nfast > 0) {
                 if (qa > 0) generic(p0, p0 + qa - 1);
-                fast_pairs_f32(reinterpret_cast<const RowF32 *>(tabp), (u32)cb, (u32)(cb >> 32),
-                               strm, rk, o + (2 * p0 - poff), (u32)qa, (u32)(qa + nfast), bb,
-                               (u32)(lo + 1), avg, par, lane);
+                i64 *ob = o + (2 * p0 - poff);
+                const u32 fa = (u32)qa, fb = (u32)(qa + nfast), l1 = (u32)(lo + 1);
+                if constexpr (sizeof(RowT) == 8) {
+                    fast_pairs_f32(reinterpret_cast<const RowF32 *>(tabp), (u32)cb, (u32)(cb >> 32),
+                                   strm, rk, ob, fa, fb, bb, l1, avg, par, lane);
+                } else if constexpr (SMODE == 2) {
+                    const SoA64View v{stw, sal};
+                    if (par) fast_pairs_f64_p<SoA64View, 1>(v, (u32)cb, (u32)(cb >> 32), strm, rk, ob, fa, fb, bb, l1, avg, lane);
+                    else fast_pairs_f64_p<SoA64View, 0>(v, (u32)cb, (u32)(cb >> 32), strm, rk, ob, fa, fb, bb, l1, avg, lane);
+                } else {
+                    const RowF64 *v = reinterpret_cast<const RowF64 *>(tabp);
+                    if (par) fast_pairs_f64_p<const RowF64 *, 1>(v, (u32)cb, (u32)(cb >> 32), strm, rk, ob, fa, fb, bb, l1, avg, lane);
+                    else fast_pairs_f64_p<const RowF64 *, 0>(v, (u32)cb, (u32)(cb >> 32), strm, rk, ob, fa, fb, bb, l1, avg, lane);
+                }
                 if (qa + nfast < np) generic(p0 + qa + nfast, p1);
                 continue;
             }
