@@ -191,15 +191,15 @@ def fast_section_reference(tw, al, avg, lo, span, seed, strm, ctr0, m):
     return O.rule(tw, al, avg, u, lo, span)
 
 
-@pytest.mark.parametrize("ctr0,dtype", [(0, torch.float32), (5, torch.float32),
-                                        (2**32 - 3, torch.float32), (7, torch.float64)])
-def test_fast_rng_sectioned_bit_exact(ctr0, dtype):
+@pytest.mark.parametrize("ctr0,dtype,S", [(0, torch.float32, 4096), (5, torch.float32, 4096),
+                                          (2**32 - 3, torch.float32, 4096), (7, torch.float64, 1 << 14),
+                                          (3, torch.float64, 4096)])
+def test_fast_rng_sectioned_bit_exact(ctr0, dtype, S):
     """rng="philox4x32": the sectioned kernel (interior fast path, checked
-    edges, misaligned 16-byte stores, several passes per call; f64 rows with
-    2^14-row sections staged as threshold/alias arrays) against a numpy
-    restatement of the GPU-native stream."""
+    edges, misaligned outputs, several passes per call; f64 rows staged as
+    rows (S=4096) or, for 2^14-row sections, as threshold/alias arrays)
+    against a numpy restatement of the GPU-native stream."""
     g = np.random.default_rng(ctr0 + 1)
-    S = 4096 if dtype == torch.float32 else 1 << 14
     n, M = 3 * S + 1000, 1_500_003
     w = (g.random(n) + 1e-3).astype(np.float32 if dtype == torch.float32 else np.float64)
     ws = ak.make_weight_set(torch.from_numpy(w).to(DEV))
