@@ -36,6 +36,8 @@ struct BlockInfo {
     int jt;         // terminal heavy (-1: no pairing); heavies (jt, nh) forwarded
     u32 cur;        // 1: heavy jt forwarded with residual curw
     u32 nres;       // forwarded items
+    u32 pL, pH;     // block offsets of the first forwarded light / heavy (len: none)
+    u32 pT;         // block offset of the forwarded terminal heavy (~0: none)
     double curw;
     u64 nwritten;   // rows written by the block
 };
@@ -71,46 +73,91 @@ __device__ __forceinline__ void block_scan2(u32 a, u32 b, u32 &ea, u32 &eb, u32 
     __syncthreads();
 }
 
-// exclusive block scan of a double (thread-order association, deterministic)
-__device__ __forceinline__ double block_scan_d(double x, double &total)
-{
-    __shared__ double sd[PP_TB / 32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    double inc = x;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const double y = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc = inc + y;
-    }
-    if (lane == 31) sd[wid] = inc;
-    __syncthreads();
-    double off = 0.0;
-    total = 0.0;
-    for (int k = 0; k < PP_TB / 32; ++k) {
-        if (k < wid) off = off + sd[k];
-        total = total + sd[k];
-    }
-    __syncthreads();
-    return off + (inc - x);
-}
-
-// dynamic shared memory of a block of bs items: item offsets (lights from
-// the front, heavies from the back), weights, keys (+1 for DL(nl))
-struct PPSmem {
-    u32 *item;
-    double *wt;
+// Dynamic shared memory of a block of bs items: the raw weights (staged
+// once), the class-compacted keys (logical index: lights [0, nl] with DL(nl)
+// at nl, heavies from nl + 1; stored at pk(x) = x + x/8 so that a lane's 8
+// consecutive keys are bank-conflict free) and block offsets (lights [0, nl),
+// heavies from nl).  Per-(row, warp) class counts and offsets are static.
+constexpr int PP_MAXR = (11000 + PP_TB - 1) / PP_TB;  // rows of PP_TB items per block
+__host__ __device__ __forceinline__ u32 pk(u32 x) { return x + (x >> 3); }
+template <typename T> struct PPSmem {
+    T *sw;
     double *key;
+    unsigned short *item;
 };
-__device__ __forceinline__ PPSmem pp_smem(unsigned char *base, u32 bs)
+template <typename T> __device__ __forceinline__ PPSmem<T> pp_smem(unsigned char *base, u32 bs)
 {
-    PPSmem S;
-    S.wt = reinterpret_cast<double *>(base);
-    S.key = S.wt + bs;
-    S.item = reinterpret_cast<u32 *>(S.key + bs + 1);
+    PPSmem<T> S;
+    S.sw = reinterpret_cast<T *>(base);
+    S.key = reinterpret_cast<double *>(base + (((size_t)bs * sizeof(T) + 15) & ~(size_t)15));
+    S.item = reinterpret_cast<unsigned short *>(S.key + pk(bs + 2) + 1);
     return S;
 }
 
-// lights: slots [0, nl); heavies: slot nl + j
+// In-place monotone prefix over the logical keys [a0, a0 + cnt) (exclusive
+// or inclusive), in item order.  Chunks of 256 (lane l: 8 consecutive keys)
+// go to the warps round-robin: each lane forms its sequential local prefix,
+// a warp scan (Kogge-Stone, then a running max) of the lane totals gives the
+// lane offsets, and every value is clamped to its lane's upper bound, so the
+// chunk-local values are non-decreasing and end at the chunk total.  Chunk
+// offsets are then the sequential sums of the chunk totals.  Every step adds
+// a non-negative term to a non-decreasing value (or clamps), so the keys are
+// non-decreasing throughout (the merge needs sorted keys).  Returns the total.
+__device__ __forceinline__ double block_prefix(double *key, u32 a0, u32 cnt, bool exclusive)
+{
+    __shared__ double ctot[PP_MAXR + 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const u32 C = (cnt + 255) / 256;
+    for (u32 c = wid; c < C; c += PP_TB / 32) {
+        const u32 e0 = c * 256 + lane * 8;
+        double v[8], s = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const double x = e0 + q < cnt ? key[pk(a0 + e0 + q)] : 0.0;
+            if (exclusive) { v[q] = s; s = s + x; }
+            else { s = s + x; v[q] = s; }
+        }
+        double inc = s;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc = inc + y;
+        }
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc = inc > y ? inc : y;
+        }
+        double ex = __shfl_up_sync(0xffffffffu, inc, 1);
+        if (lane == 0) ex = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (e0 + q < cnt) {
+                const double x = ex + v[q];
+                key[pk(a0 + e0 + q)] = x < inc ? x : inc;
+            }
+        }
+        if (lane == 31) ctot[c] = inc;
+    }
+    __syncthreads();
+    double tot = 0.0;
+    for (u32 c = 0; c < C; ++c) tot = tot + ctot[c];
+    for (u32 c = wid; c < C; c += PP_TB / 32) {
+        double off = 0.0;
+        for (u32 k = 0; k < c; ++k) off = off + ctot[k];
+        const u32 e0 = c * 256 + lane * 8;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (e0 + q < cnt) key[pk(a0 + e0 + q)] = off + key[pk(a0 + e0 + q)];
+    }
+    __syncthreads();
+    return tot;
+}
+
+// Per block: stage the weights (bulk async copy), classify by warp ballots, place
+// lights and heavies in item order (rank = offset of the (row, warp) + rank
+// in the ballot), prefix keys, then one merge path over the two key
+// sequences writes every handled row (heavy first on ties: DH <= DL).
 template <typename T>
 __global__ void __launch_bounds__(PP_TB) k_prepack_block(const T *__restrict__ w, u64 n, double avg,
                                                          u32 bs, u32 thr,
@@ -121,41 +168,85 @@ __global__ void __launch_bounds__(PP_TB) k_prepack_block(const T *__restrict__ w
     typedef decltype(RowT::tw) TwT;
     typedef decltype(RowT::alias) AliasT;
     extern __shared__ __align__(16) unsigned char pp_raw[];
-    PPSmem S = pp_smem(pp_raw, bs);
+    const PPSmem<T> S = pp_smem<T>(pp_raw, bs);
+    __shared__ u32 s_cnt[2][PP_MAXR * (PP_TB / 32)];
     __shared__ u64 s_written;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const u32 lt = (1u << lane) - 1u;
     const u64 b0 = (u64)blockIdx.x * bs;
     const u32 len = (u32)(b0 + bs <= n ? bs : n - b0);
-    const u32 per = (len + PP_TB - 1) / PP_TB;
-    const u32 i0 = threadIdx.x * per, i1 = i0 + per < len ? i0 + per : len;
-    if (threadIdx.x == 0) s_written = 0;
-    // classify; exactly-full items are final at once
-    u32 cl = 0, ch = 0, cw = 0;
-    for (u32 i = i0; i < i1; ++i) {
-        const int c = item_class(w[b0 + i], avg);
-        cl += c == 0;
-        ch += c == 1;
-        if (c == 2) {
-            RowT row;
-            row.tw = (TwT)w[b0 + i];
-            row.alias = (AliasT)(b0 + i + 1);
-            rows[b0 + i] = row;
-            ++cw;
+    const u32 R = (len + PP_TB - 1) / PP_TB;
+    const u32 E = R * (PP_TB / 32);
+    // stage the block's weights: one bulk async copy (TMA) when aligned
+    __shared__ __align__(8) u64 bar;
+    const T *src = w + b0;
+    const u32 bytes = len * (u32)sizeof(T);
+    const bool bulk = ((((uintptr_t)src) | bytes) & 15) == 0;
+    if (threadIdx.x == 0) {
+        s_written = 0;
+        if (bulk) {
+            mbar_init(&bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            mbar_expect_tx(&bar, bytes);
+            bulk_g2s(S.sw, src, bytes, &bar);
         }
     }
-    u32 el, eh, nl, nh;
-    block_scan2(cl, ch, el, eh, nl, nh);
+    if (bulk) {
+        __syncthreads();  // the barrier is initialised before anyone waits on it
+        mbar_wait(&bar, 0);
+    } else {
+        for (u32 i = threadIdx.x; i < len; i += PP_TB) S.sw[i] = src[i];
+        __syncthreads();
+    }
+    // count per (row, warp); exactly-full items are final at once
+    u32 cw = 0;
+    for (u32 r = 0; r < R; ++r) {
+        const u32 i = r * PP_TB + threadIdx.x;
+        int c = 3;
+        if (i < len) {
+            const T v = S.sw[i];
+            c = item_class(v, avg);
+            if (c == 2) {
+                RowT row;
+                row.tw = (TwT)v;
+                row.alias = (AliasT)(b0 + i + 1);
+                rows[b0 + i] = row;
+                ++cw;
+            }
+        }
+        const unsigned lb = __ballot_sync(0xffffffffu, c == 0), hb = __ballot_sync(0xffffffffu, c == 1);
+        if (lane == 0) {
+            s_cnt[0][r * (PP_TB / 32) + wid] = __popc(lb);
+            s_cnt[1][r * (PP_TB / 32) + wid] = __popc(hb);
+        }
+    }
+    __syncthreads();
+    u32 nl, nh;
+    {
+        // exclusive offsets of the (row, warp) counts, in item order
+        const u32 e0 = 2 * threadIdx.x, e1 = e0 + 1;
+        const u32 l0 = e0 < E ? s_cnt[0][e0] : 0, l1 = e1 < E ? s_cnt[0][e1] : 0;
+        const u32 h0 = e0 < E ? s_cnt[1][e0] : 0, h1 = e1 < E ? s_cnt[1][e1] : 0;
+        u32 el, eh;
+        block_scan2(l0 + l1, h0 + h1, el, eh, nl, nh);
+        if (e0 < E) { s_cnt[0][e0] = el; s_cnt[1][e0] = eh; }
+        if (e1 < E) { s_cnt[0][e1] = el + l0; s_cnt[1][e1] = eh + h0; }
+    }
     if (cw) atomicAdd((unsigned long long *)&s_written, (unsigned long long)cw);
-    for (u32 i = i0; i < i1; ++i) {
-        const T v = w[b0 + i];
-        const int c = item_class(v, avg);
+    __syncthreads();
+    // class-compacted terms (avg - w for lights, w - avg for heavies) and offsets
+    for (u32 r = 0; r < R; ++r) {
+        const u32 i = r * PP_TB + threadIdx.x;
+        const int c = i < len ? item_class(S.sw[i], avg) : 3;
+        const unsigned lb = __ballot_sync(0xffffffffu, c == 0), hb = __ballot_sync(0xffffffffu, c == 1);
         if (c == 0) {
-            S.item[el] = i;
-            S.wt[el] = (double)v;
-            ++el;
+            const u32 k = s_cnt[0][r * (PP_TB / 32) + wid] + __popc(lb & lt);
+            S.key[pk(k)] = avg - (double)S.sw[i];
+            S.item[k] = (unsigned short)i;
         } else if (c == 1) {
-            S.item[nl + eh] = i;
-            S.wt[nl + eh] = (double)v;
-            ++eh;
+            const u32 j = s_cnt[1][r * (PP_TB / 32) + wid] + __popc(hb & lt);
+            S.key[pk(nl + 1 + j)] = (double)S.sw[i] - avg;
+            S.item[nl + j] = (unsigned short)i;
         }
     }
     __syncthreads();
@@ -165,44 +256,19 @@ __global__ void __launch_bounds__(PP_TB) k_prepack_block(const T *__restrict__ w
     double curw = 0.0;
     u64 nwritten = 0;
     if (pair) {
-        // keys: DL exclusive over lights, DH inclusive over heavies
-        {
-            const u32 pl = (nl + PP_TB - 1) / PP_TB, a0 = threadIdx.x * pl;
-            const u32 a1 = a0 + pl < nl ? a0 + pl : nl;
-            double s = 0.0;
-            for (u32 k = a0; k < a1; ++k) s = s + (avg - S.wt[k]);
-            double tot;
-            double x = block_scan_d(s, tot);
-            for (u32 k = a0; k < a1; ++k) {
-                S.key[k] = x;
-                x = x + (avg - S.wt[k]);
-            }
-            (void)tot;
-            if (a0 < a1 && a1 == nl) S.key[nl] = x;  // DL(nl): the block's whole deficit
-        }
-        __syncthreads();
-        const double DLtot = S.key[nl];
-        {
-            const u32 ph = (nh + PP_TB - 1) / PP_TB, a0 = threadIdx.x * ph;
-            const u32 a1 = a0 + ph < nh ? a0 + ph : nh;
-            double s = 0.0;
-            for (u32 j = a0; j < a1; ++j) s = s + (S.wt[nl + j] - avg);
-            double tot;
-            double x = block_scan_d(s, tot);
-            for (u32 j = a0; j < a1; ++j) {
-                x = x + (S.wt[nl + j] - avg);
-                S.key[nl + 1 + j] = x;  // heavy keys after DL(nl)
-            }
-        }
-        __syncthreads();
-        const double *DL = S.key;           // [0, nl]
-        const double *DH = S.key + nl + 1;  // [0, nh)
+        // keys: DL exclusive over lights (DL(nl) = the whole deficit), DH inclusive
+        const double DLtot = block_prefix(S.key, 0, nl, true);
+        if (threadIdx.x == 0) S.key[pk(nl)] = DLtot;
+        block_prefix(S.key, nl + 1, nh, false);
+        const double *key = S.key;
+        auto DL = [&](u32 k) { return key[pk(k)]; };           // [0, nl]
+        auto DH = [&](u32 j) { return key[pk(nl + 1 + j)]; };  // [0, nh)
         // lights absorbed before the sweep stops: #lights with DL < DH(j)
         auto lights_below = [&](double x) {
             u32 a = 0, b = nl;  // first k with DL(k) >= x
             while (a < b) {
                 const u32 m = (a + b) >> 1;
-                if (DL[m] < x) a = m + 1;
+                if (DL(m) < x) a = m + 1;
                 else b = m;
             }
             return a;
@@ -211,19 +277,19 @@ __global__ void __launch_bounds__(PP_TB) k_prepack_block(const T *__restrict__ w
             u32 a = 0, b = nh;  // first j with DH(j) > x
             while (a < b) {
                 const u32 m = (a + b) >> 1;
-                if (DH[m] <= x) a = m + 1;
+                if (DH(m) <= x) a = m + 1;
                 else b = m;
             }
             return a;
         };
-        if (DH[nh - 1] <= DLtot) {
+        if (DH(nh - 1) <= DLtot) {
             jt = (int)nh - 1;
-            kend = lights_below(DH[nh - 1]);
+            kend = lights_below(DH(nh - 1));
         } else {
             kend = nl;
             jt = (int)heavies_upto(DLtot);
         }
-        const double wt_end = (DH[jt] - DL[kend]) + avg;
+        const double wt_end = (DH(jt) - DL(kend)) + avg;
         cur = wt_end == avg ? 0u : 1u;
         curw = wt_end;
         if (fabs(wt_end - avg) <= 1e-9 * avg) {
@@ -235,18 +301,20 @@ __global__ void __launch_bounds__(PP_TB) k_prepack_block(const T *__restrict__ w
             __shared__ int s_j;
             __shared__ double s_w;
             if (threadIdx.x == 0) {
+                auto wl = [&](u32 k) { return (double)S.sw[S.item[k]]; };
+                auto wh = [&](u32 j) { return (double)S.sw[S.item[nl + j]]; };
                 u32 k = 0;
                 int j = 0;
-                double wc = S.wt[nl];
+                double wc = wh(0);
                 while (true) {
                     if (wc > avg) {
                         if (k == nl) break;
                         const u64 it = b0 + S.item[k];
                         RowT row;
-                        row.tw = (TwT)w[it];
+                        row.tw = (TwT)S.sw[S.item[k]];
                         row.alias = (AliasT)(b0 + S.item[nl + j] + 1);
                         rows[it] = row;
-                        wc += S.wt[k] - avg;
+                        wc += wl(k) - avg;
                         ++k;
                     } else {
                         if ((u32)j + 1 >= nh) break;
@@ -254,7 +322,7 @@ __global__ void __launch_bounds__(PP_TB) k_prepack_block(const T *__restrict__ w
                         row.tw = tw_store<T>(wc, avg);
                         row.alias = (AliasT)(b0 + S.item[nl + j + 1] + 1);
                         rows[b0 + S.item[nl + j]] = row;
-                        wc += S.wt[nl + j + 1] - avg;
+                        wc += wh(j + 1) - avg;
                         ++j;
                     }
                 }
@@ -276,34 +344,55 @@ __global__ void __launch_bounds__(PP_TB) k_prepack_block(const T *__restrict__ w
             jt = s_j;
             cur = s_cur;
             curw = s_w;
-            nwritten = (u64)kend + (u64)jt + (cur ? 0 : 1);
         } else {
-        // lights [0, kend): alias = first heavy with DH > DL(k)
-        for (u32 k = threadIdx.x; k < kend; k += PP_TB) {
-            const u32 j = heavies_upto(DL[k]);
-            const u64 it = b0 + S.item[k];
-            RowT row;
-            row.tw = (TwT)w[it];
-            row.alias = (AliasT)(b0 + S.item[nl + j] + 1);
-            rows[it] = row;
-        }
-        // heavies [0, jt): close at DH(j) + avg - DL(#lights below DH(j))
-        for (u32 j = threadIdx.x; j < (u32)jt; j += PP_TB) {
-            const u32 k = lights_below(DH[j]);
-            RowT row;
-            row.tw = tw_store<T>((DH[j] - DL[k]) + avg, avg);
-            row.alias = (AliasT)(b0 + S.item[nl + j + 1] + 1);
-            rows[b0 + S.item[nl + j]] = row;
-        }
-        if (threadIdx.x == 0 && !cur) {
-            const u64 it = b0 + S.item[nl + jt];
-            RowT row;
-            row.tw = tw_store<T>(wt_end, avg);
-            row.alias = (AliasT)(it + 1);
-            rows[it] = row;
+            // merge path over lights [0, nl) and heavies [0, nh): thread t
+            // takes merged positions [t per, (t + 1) per); a taken light k
+            // (k < kend) aliases the next heavy, a taken heavy j (j < jt)
+            // closes against the lights taken before it
+            const u32 total = nl + nh;
+            const u32 per = (total + PP_TB - 1) / PP_TB;
+            const u32 d0 = threadIdx.x * per;
+            if (d0 < total) {
+                const u32 lo0 = d0 > nh ? d0 - nh : 0, hi0 = d0 < nl ? d0 : nl;
+                u32 lo = lo0, hi = hi0;  // greatest i with light i-1 before heavy d0-i
+                while (lo < hi) {
+                    const u32 m = (lo + hi + 1) >> 1;
+                    if (d0 - m >= nh || DL(m - 1) < DH(d0 - m)) lo = m;
+                    else hi = m - 1;
+                }
+                u32 k = lo, j = d0 - lo;
+                const u32 steps = d0 + per < total ? per : total - d0;
+                for (u32 d = 0; d < steps; ++d) {
+                    const bool take_h = j < nh && (k >= nl || DH(j) <= DL(k));
+                    if (take_h) {
+                        if (j < (u32)jt) {
+                            RowT row;
+                            row.tw = tw_store<T>((DH(j) - DL(k)) + avg, avg);
+                            row.alias = (AliasT)(b0 + S.item[nl + j + 1] + 1);
+                            rows[b0 + S.item[nl + j]] = row;
+                        }
+                        ++j;
+                    } else {
+                        if (k < kend) {
+                            const u32 it = S.item[k];
+                            RowT row;
+                            row.tw = (TwT)S.sw[it];
+                            row.alias = (AliasT)(b0 + S.item[nl + j] + 1);
+                            rows[b0 + it] = row;
+                        }
+                        ++k;
+                    }
+                }
+            }
+            if (threadIdx.x == 0 && !cur) {
+                const u64 it = b0 + S.item[nl + jt];
+                RowT row;
+                row.tw = tw_store<T>(wt_end, avg);
+                row.alias = (AliasT)(it + 1);
+                rows[it] = row;
+            }
         }
         nwritten = (u64)kend + (u64)jt + (cur ? 0 : 1);
-        }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -316,11 +405,20 @@ __global__ void __launch_bounds__(PP_TB) k_prepack_block(const T *__restrict__ w
         bi.curw = curw;
         bi.nres = (nl - kend) + (u32)((int)nh - (jt + 1)) + (pair ? cur : 0u);
         bi.nwritten = s_written + nwritten;
+        // forwarded items: the lights from rank kend and the heavies from
+        // rank jt + 1 (jt itself when it carries a residual), in item order
+        const u32 hf = (u32)(jt + 1) - (pair && cur ? 1u : 0u);
+        bi.pL = kend < nl ? S.item[kend] : len;
+        bi.pH = hf < nh ? S.item[nl + hf] : len;
+        bi.pT = pair && cur ? S.item[nl + jt] : 0xFFFFFFFFu;
         info[blockIdx.x] = bi;
     }
 }
 
-// residual items of each block in item order at res_off[block] + ...
+// Residual items of each block in item order at res_off[block] + ...: the
+// lights at block offsets >= pL and the heavies at offsets >= pH (the
+// terminal heavy at pT with its residual weight), i.e. only the block's tail
+// from min(pL, pH) is visited.
 template <typename T>
 __global__ void __launch_bounds__(PP_TB) k_prepack_emit(const T *__restrict__ w, u64 n, double avg,
                                                         u32 bs, const BlockInfo *__restrict__ info,
@@ -328,50 +426,39 @@ __global__ void __launch_bounds__(PP_TB) k_prepack_emit(const T *__restrict__ w,
                                                         i64 *__restrict__ res_idx,
                                                         double *__restrict__ res_w)
 {
+    __shared__ u32 s_wc[PP_TB / 32];
     const BlockInfo bi = info[blockIdx.x];
     if (bi.nres == 0) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const u64 b0 = (u64)blockIdx.x * bs;
     const u32 len = (u32)(b0 + bs <= n ? bs : n - b0);
-    const u32 per = (len + PP_TB - 1) / PP_TB;
-    const u32 i0 = threadIdx.x * per, i1 = i0 + per < len ? i0 + per : len;
-    u32 cl = 0, ch = 0;
-    for (u32 i = i0; i < i1; ++i) {
-        const int c = item_class(w[b0 + i], avg);
-        cl += c == 0;
-        ch += c == 1;
-    }
-    u32 el, eh, tl, th;
-    block_scan2(cl, ch, el, eh, tl, th);
-    // forwarded flag per item, then a second scan for positions
-    auto fwd = [&](int c, u32 lr, u32 hr) {
-        if (c == 0) return lr >= bi.kend;
-        if (c == 1) return (int)hr > bi.jt || ((int)hr == bi.jt && bi.cur);
-        return false;
-    };
-    u32 cf = 0;
-    {
-        u32 lr = el, hr = eh;
-        for (u32 i = i0; i < i1; ++i) {
-            const int c = item_class(w[b0 + i], avg);
-            cf += fwd(c, lr, hr);
-            lr += c == 0;
-            hr += c == 1;
+    const u32 p0 = bi.pL < bi.pH ? bi.pL : bi.pH;
+    i64 pos = res_off[blockIdx.x];
+    for (u32 base = p0; base < len; base += PP_TB) {
+        const u32 i = base + threadIdx.x;
+        bool f = false;
+        T v = T(0);
+        if (i < len) {
+            v = w[b0 + i];
+            const int c = item_class(v, avg);
+            f = (c == 0 && i >= bi.pL) || (c == 1 && i >= bi.pH);
         }
-    }
-    u32 ef, dummy, tf, td;
-    block_scan2(cf, 0u, ef, dummy, tf, td);
-    i64 pos = res_off[blockIdx.x] + ef;
-    u32 lr = el, hr = eh;
-    for (u32 i = i0; i < i1; ++i) {
-        const T v = w[b0 + i];
-        const int c = item_class(v, avg);
-        if (fwd(c, lr, hr)) {
-            res_idx[pos] = (i64)(b0 + i + 1);
-            res_w[pos] = (c == 1 && (int)hr == bi.jt) ? bi.curw : (double)v;
-            ++pos;
+        const unsigned fb = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) s_wc[wid] = __popc(fb);
+        __syncthreads();
+        u32 before = 0, all = 0;
+#pragma unroll
+        for (int k = 0; k < PP_TB / 32; ++k) {
+            before += k < wid ? s_wc[k] : 0u;
+            all += s_wc[k];
         }
-        lr += c == 0;
-        hr += c == 1;
+        if (f) {
+            const i64 q = pos + before + __popc(fb & ((1u << lane) - 1u));
+            res_idx[q] = (i64)(b0 + i + 1);
+            res_w[q] = i == bi.pT ? bi.curw : (double)v;
+        }
+        pos += all;
+        __syncthreads();
     }
 }
 
@@ -429,7 +516,7 @@ __global__ void k_residual_remap(const RowF64 *__restrict__ rt, const i64 *__res
     rows[res_idx[r] - 1] = o;
 }
 
-size_t pp_smem_bytes(u32 bs) { return (size_t)bs * 8 + (size_t)(bs + 1) * 8 + (size_t)bs * 4 + 16; }
+size_t pp_smem_bytes(u32 bs, size_t wb) { return (((size_t)bs * wb + 15) & ~(size_t)15) + (size_t)(pk(bs + 2) + 1) * 8 + (size_t)bs * 2 + 16; }
 
 inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -453,8 +540,8 @@ int ak_greedy_prepack(const void *w, int dtype, uint64_t n, double avg, uint32_t
 {
     if (n == 0) return AK_ERR_EMPTY_INPUT;
     if (block_size < 2 || threshold < 1) return AK_ERR_VALUE;
-    const size_t smem = pp_smem_bytes(block_size);
-    if (smem > 220 * 1024) return AK_ERR_VALUE;  // block does not fit in shared memory
+    const size_t smem = pp_smem_bytes(block_size, dtype == AK_F32 ? 4 : 8);
+    if (smem > 220 * 1024 || block_size > 11000) return AK_ERR_VALUE;  // block does not fit
     if (ws_bytes < ak_prepack_workspace_bytes(n, block_size)) return AK_ERR_WORKSPACE;
     cudaStream_t st = ak_stream(stream);
     const u64 nb = (n + block_size - 1) / block_size;

@@ -1,6 +1,7 @@
 """Time psa_construct (CUDA events, device-resident weights) at one size.
 
     python tools/time_build.py [--n 1e9] [--dist uniform|zipf] [--dtype float32|float64] [--reps 10]
+                               [--method psa|psa_plus]
 """
 import argparse
 import os
@@ -17,12 +18,16 @@ ap.add_argument("--n", type=float, default=1e9)
 ap.add_argument("--dist", default="uniform")
 ap.add_argument("--dtype", default="float32")
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--method", default="psa")
 a = ap.parse_args()
 N = int(a.n)
 dt = torch.float32 if a.dtype == "float32" else torch.float64
 r = ak.RngStream(1)
 ws = ak.gen_uniform(N, r, dtype=dt) if a.dist == "uniform" else ak.gen_power_law(N, 1.0, r, dtype=dt)
 t = build_table(ws)
+if a.method == "psa_plus":
+    def build_table(ws, t):  # noqa: F811
+        return ak.psa_plus_construct(ws)
 for _ in range(3):
     build_table(ws, t)
 torch.cuda.synchronize()
@@ -38,5 +43,5 @@ ts.sort()
 b = 4 if dt == torch.float32 else 8
 byts = N * (2 * b + b + 4)
 med = ts[len(ts) // 2]
-print(f"build N={N:.0e} {a.dist} {a.dtype}: median {med:.3f} ms  min {ts[0]:.3f} ms  "
+print(f"{a.method} N={N:.0e} {a.dist} {a.dtype}: median {med:.3f} ms  min {ts[0]:.3f} ms  "
       f"{N / med / 1e6:.1f} G items/s  {byts / med / 1e6:.0f} GB/s algorithmic")
