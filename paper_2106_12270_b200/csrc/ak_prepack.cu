@@ -530,7 +530,7 @@ extern "C" {
 size_t ak_prepack_workspace_bytes(uint64_t n, uint32_t block_size)
 {
     const u64 nb = block_size ? (n + block_size - 1) / block_size : 0;
-    return al256(nb * sizeof(BlockInfo)) + 2 * al256((nb + 1) * 8) + 256 + 2 * al256(n * 8);
+    return al256(nb * sizeof(BlockInfo)) + 2 * al256((nb + 1) * 8) + 256;
 }
 
 int ak_greedy_prepack(const void *w, int dtype, uint64_t n, double avg, uint32_t block_size,
