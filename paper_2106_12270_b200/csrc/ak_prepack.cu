@@ -239,14 +239,12 @@ __global__ void __launch_bounds__(PP_TB) k_prepack_block(const T *__restrict__ w
         const u32 i = r * PP_TB + threadIdx.x;
         const int c = i < len ? item_class(S.sw[i], avg) : 3;
         const unsigned lb = __ballot_sync(0xffffffffu, c == 0), hb = __ballot_sync(0xffffffffu, c == 1);
-        if (c == 0) {
-            const u32 k = s_cnt[0][r * (PP_TB / 32) + wid] + __popc(lb & lt);
-            S.key[pk(k)] = avg - (double)S.sw[i];
-            S.item[k] = (unsigned short)i;
-        } else if (c == 1) {
-            const u32 j = s_cnt[1][r * (PP_TB / 32) + wid] + __popc(hb & lt);
-            S.key[pk(nl + 1 + j)] = (double)S.sw[i] - avg;
-            S.item[nl + j] = (unsigned short)i;
+        if (c < 2) {  // one store path for both classes (no divergence)
+            const bool l = c == 0;
+            const u32 rk = s_cnt[l ? 0 : 1][r * (PP_TB / 32) + wid] + __popc((l ? lb : hb) & lt);
+            const double x = (double)S.sw[i] - avg;
+            S.key[pk(l ? rk : nl + 1 + rk)] = l ? -x : x;  // avg - w == -(w - avg) exactly
+            S.item[l ? rk : nl + rk] = (unsigned short)i;
         }
     }
     __syncthreads();
@@ -362,25 +360,28 @@ __global__ void __launch_bounds__(PP_TB) k_prepack_block(const T *__restrict__ w
                 }
                 u32 k = lo, j = d0 - lo;
                 const u32 steps = d0 + per < total ? per : total - d0;
+                // one row per step on a single (branch-free) path: a taken
+                // heavy j closes against DL(k), a taken light k aliases heavy j
+                double dh = j < nh ? DH(j) : 0.0, dl = DL(k < nl ? k : nl);
                 for (u32 d = 0; d < steps; ++d) {
-                    const bool take_h = j < nh && (k >= nl || DH(j) <= DL(k));
+                    const bool take_h = j < nh && (k >= nl || dh <= dl);
+                    const u32 self = take_h ? nl + j : k;
+                    const u32 it = S.item[self < nl + nh ? self : 0];
+                    const u32 al = S.item[take_h ? (nl + j + 1 < nl + nh ? nl + j + 1 : nl + j) : nl + (j < nh ? j : 0)];
+                    const bool wr = take_h ? j < (u32)jt : k < kend;
+                    // only a closing heavy's value is <= avg (+ rounding); any other
+                    // step passes avg, as tw_store walks values above avg down
+                    const TwT hv = tw_store<T>(take_h && wr ? (dh - dl) + avg : avg, avg);
+                    RowT row;
+                    row.tw = take_h ? hv : (TwT)S.sw[it];
+                    row.alias = (AliasT)(b0 + al + 1);
+                    if (wr) rows[b0 + it] = row;
                     if (take_h) {
-                        if (j < (u32)jt) {
-                            RowT row;
-                            row.tw = tw_store<T>((DH(j) - DL(k)) + avg, avg);
-                            row.alias = (AliasT)(b0 + S.item[nl + j + 1] + 1);
-                            rows[b0 + S.item[nl + j]] = row;
-                        }
                         ++j;
+                        dh = j < nh ? DH(j) : 0.0;
                     } else {
-                        if (k < kend) {
-                            const u32 it = S.item[k];
-                            RowT row;
-                            row.tw = (TwT)S.sw[it];
-                            row.alias = (AliasT)(b0 + S.item[nl + j] + 1);
-                            rows[b0 + it] = row;
-                        }
                         ++k;
+                        dl = DL(k < nl ? k : nl);
                     }
                 }
             }
