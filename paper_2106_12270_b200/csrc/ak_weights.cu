@@ -8,8 +8,10 @@
 // against np.sum by tests).  The tree depends on n only, so the device
 // evaluates exactly the same additions in the same order — the total is
 // bit-identical to the reference's — with every subtree of the cut at depth D
-// summed by one thread and the top D levels combined by two more launches.
+// summed by one warp (k_pairwise_leaves) and the top D levels combined by one
+// or two more launches.
 #include "ak_common.cuh"
+#include <math_constants.h>
 
 namespace {
 
@@ -124,23 +126,143 @@ __device__ double subtree_sum(const T *a, u64 off, u64 n)
     return vals[0];
 }
 
-template <typename T>
-__global__ void k_pairwise_leaves(const T *__restrict__ w, u64 n, int D, double *__restrict__ part,
-                                  unsigned long long *__restrict__ first_bad)
+// One warp per node of the cut (<= ~2300 values).  Lane l takes the node's
+// descendant slot l at depth 5 below it: every leaf of the node (<= 128
+// values) sits in exactly one slot (its leftmost), because no descendant at
+// depth 5 exceeds 128 values.  The leaves are summed four at a time, one
+// 8-lane group per leaf with lane k holding numpy's accumulator r_k (a warp
+// load touches four 32-byte runs), the groups fold their accumulators in
+// numpy's order and add the tail values; then the five levels above the
+// slots are folded by shuffles, each internal node adding its right child to
+// its left.  Every addition is numpy's, in its order: the sum is
+// bit-identical.  Validation (finite, > 0) rides on the same loads.
+constexpr int PW_WARPS = 4;
+constexpr int PW_SLOT_DEPTH = 5;
+
+// descendant of `root` at relative depth d, index idx (MSB first: 0 = left)
+__device__ __forceinline__ Node node_below(Node root, int d, u32 idx)
 {
-    u64 idx = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (1ull << D)) return;
-    Node nd = node_at(n, D, idx);
-    if (!nd.exists) return;
-    // validation of this node's range: finite and > 0 (model.py:101-104)
-    for (u64 i = nd.off; i < nd.off + nd.size; ++i) {
-        double v = ld_val(w, i);
-        if (!(isfinite(v) && v > 0.0)) {
-            atomicMin(first_bad, (unsigned long long)i);
-            break;
+    Node nd = root;
+    for (int lvl = 0; lvl < d; ++lvl) {
+        const int bit = (int)((idx >> (d - 1 - lvl)) & 1);
+        if (nd.size <= PW_BLOCK) {
+            if (bit) {
+                nd.exists = false;
+                return nd;
+            }
+            continue;
+        }
+        const u64 h = split_point(nd.size);
+        if (bit == 0) nd.size = h;
+        else {
+            nd.off += h;
+            nd.size -= h;
         }
     }
-    part[idx] = nd.leaf ? leaf_sum(w, nd.off, nd.size) : subtree_sum(w, nd.off, nd.size);
+    nd.leaf = nd.size <= PW_BLOCK;
+    return nd;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(PW_WARPS * 32) k_pairwise_leaves(const T *__restrict__ w, u64 n, int D,
+                                                                   double *__restrict__ part,
+                                                                   unsigned long long *__restrict__ first_bad)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const u64 idx = (u64)blockIdx.x * PW_WARPS + wid;
+    if (idx >= (1ull << D)) return;
+    const Node nd = node_at(n, D, idx);
+    if (!nd.exists) return;
+    if (nd.size > 32 * PW_BLOCK) {  // cut nodes are <= ~2300 values; n > 2^41 only
+        if (lane == 0) {
+            for (u64 i = nd.off; i < nd.off + nd.size; ++i) {
+                const double v = ld_val(w, i);
+                if (!(isfinite(v) && v > 0.0)) {
+                    atomicMin(first_bad, (unsigned long long)i);
+                    break;
+                }
+            }
+            part[idx] = nd.size <= PW_BLOCK ? leaf_sum(w, nd.off, nd.size) : subtree_sum(w, nd.off, nd.size);
+        }
+        return;
+    }
+    const Node mine = node_below(nd, PW_SLOT_DEPTH, (u32)lane);  // a leaf or nothing
+    const u32 myoff = (u32)(mine.off - nd.off), mylen = mine.exists ? (u32)mine.size : 0u;
+    const int g = lane >> 3, k = lane & 7;
+    u64 bad = ~0ull;
+    double leafsum = 0.0;
+    for (int s0 = 0; s0 < 32; s0 += 4) {
+        const int sl = s0 + g;  // slot handled by this group
+        const u32 off = __shfl_sync(0xffffffffu, myoff, sl);
+        const u32 len = __shfl_sync(0xffffffffu, mylen, sl);
+        const u64 base = nd.off + off;
+        const u32 m8 = len >= 8 ? len - len % 8 : 0;
+        // all (<= 16) loads of the accumulator first, then its additions in order
+        double x[PW_BLOCK / 8];
+#pragma unroll
+        for (int q = 0; q < (int)(PW_BLOCK / 8); ++q) {
+            const u32 i = 8u * q + k;
+            x[q] = i < m8 ? ld_val(w, base + i) : 1.0;
+        }
+        const u32 nt = len - m8;  // tail values (< 8), lane k holds tail value k
+        const double xt = (u32)k < nt ? ld_val(w, base + m8 + k) : 1.0;
+        double r = 0.0;
+        if (len >= 8) {
+            r = x[0];
+#pragma unroll
+            for (int q = 1; q < (int)(PW_BLOCK / 8); ++q)
+                if (8u * q < m8) r += x[q];
+        }
+        // finite and > 0: a NaN or inf makes the lane's sum non-finite and a
+        // value <= 0 shows in the minimum; only then is the exact first bad
+        // index searched for (a finite sum overflowing to inf just searches)
+        double mn = xt;
+#pragma unroll
+        for (int q = 0; q < (int)(PW_BLOCK / 8); ++q) mn = fmin(mn, x[q]);
+        const bool ok = mn > 0.0 && isfinite(r + xt);
+        if (!__all_sync(0xffffffffu, ok)) {
+#pragma unroll
+            for (int q = 0; q < (int)(PW_BLOCK / 8); ++q) {
+                const u64 i = base + 8u * q + k;
+                if (!(x[q] > 0.0 && x[q] < CUDART_INF)) bad = bad < i ? bad : i;
+            }
+            if (!(xt > 0.0 && xt < CUDART_INF)) bad = bad < base + m8 + k ? bad : base + m8 + k;
+        }
+        // ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7)) within the group
+        const double s1 = r + __shfl_down_sync(0xffffffffu, r, 1);
+        const double s2 = s1 + __shfl_down_sync(0xffffffffu, s1, 2);
+        double res = s2 + __shfl_down_sync(0xffffffffu, s2, 4);
+        if (len < 8) res = 0.0;
+#pragma unroll
+        for (int j = 0; j < 7; ++j) {  // the tail, in order
+            const double v = __shfl_sync(0xffffffffu, xt, (lane & ~7) + j);
+            if ((u32)j < nt) res += v;
+        }
+        // slot sl's sum -> lane sl
+        const double got = __shfl_sync(0xffffffffu, res, (lane & 3) * 8);
+        if ((lane >> 2) == (s0 >> 2)) leafsum = got;
+    }
+    // fold the 5 levels above the slots: node (lv, t) spans slots
+    // [t 2^(5-lv), (t+1) 2^(5-lv)); its right child starts halfway
+    double v = leafsum;
+#pragma unroll
+    for (int lv = PW_SLOT_DEPTH - 1; lv >= 0; --lv) {
+        const int span = 1 << (PW_SLOT_DEPTH - lv);
+        const double o = __shfl_down_sync(0xffffffffu, v, span / 2);
+        if ((lane & (span - 1)) == 0) {
+            const Node p = node_below(nd, lv, (u32)(lane >> (PW_SLOT_DEPTH - lv)));
+            if (p.exists && !p.leaf) v = v + o;
+        }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const u64 o = __shfl_xor_sync(0xffffffffu, bad, d);
+        bad = bad < o ? bad : o;
+    }
+    if (lane == 0) {
+        if (bad != ~0ull) atomicMin(first_bad, (unsigned long long)bad);
+        part[idx] = v;
+    }
 }
 
 // Combine levels [d_lo, d_hi) in place: part holds values at depth d_hi in
@@ -206,8 +328,8 @@ int ak_weights_validate_total(const void *w, int dtype, uint64_t n, double *tota
     double *part2 = part + ((size_t)1 << D);
     AK_CUDA_TRY(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
     const u64 nthreads = 1ull << D;
-    const int tb = 128;
-    const unsigned g = (unsigned)((nthreads + tb - 1) / tb);
+    const unsigned g = (unsigned)((nthreads + PW_WARPS - 1) / PW_WARPS);
+    const int tb = PW_WARPS * 32;
     if (dtype == AK_F32)
         k_pairwise_leaves<float><<<g, tb, 0, st>>>((const float *)w, n, D, part, bad);
     else

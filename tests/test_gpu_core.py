@@ -59,7 +59,7 @@ def test_weight_set_totals_bit_identical_to_np_sum(golden, rng):
     for ci in range(len(golden["sizes"])):
         w = golden[f"c{ci}_weights"]
         assert ak.make_weight_set(w).total == float(golden[f"c{ci}_total"][0])
-    for n in (1, 7, 8, 9, 127, 128, 129, 2049, 100_003, 3_000_001):
+    for n in (1, 6, 7, 8, 9, 127, 128, 129, 1000, 2049, 65_537, 100_003, 3_000_001, 10_000_019):
         w = random_weights(rng, n, n % 5)
         assert ak.make_weight_set(w).total == float(np.sum(w))
         w32 = w.astype(np.float32)
@@ -83,6 +83,16 @@ def test_invalid_weight_first_bad_wins_at_scale():
     with pytest.raises(ak.InvalidWeight) as e:
         ak.make_weight_set(w)
     assert e.value.index == 4_000_000
+
+
+def test_invalid_weight_in_leaf_tails():
+    # bad values in a leaf's tail (n % 8 != 0) and in accumulator lanes
+    for n, pos in ((1_000_003, 1_000_002), (1_000_003, 999_999), (4099, 4098), (130, 129), (5, 3)):
+        w = torch.ones(n, dtype=torch.float32, device=DEV)
+        w[pos] = float("nan")
+        with pytest.raises(ak.InvalidWeight) as e:
+            ak.make_weight_set(w)
+        assert e.value.index == pos + 1
 
 
 def test_empty_and_shape():
