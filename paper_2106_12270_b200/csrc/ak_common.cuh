@@ -76,8 +76,15 @@ __device__ __forceinline__ RowF64 ld_row(const RowF64 *p)
 __host__ __device__ __forceinline__ float tw_to_f32(double t, double avg)
 {
     float f = (float)t;
+#ifdef __CUDA_ARCH__
+    // the walk below ends at the largest float not above avg: one conversion
+    // rounding down (avg > 0), no loop and no divergence
+    const float cap = __double2float_rd(avg);
+    return (double)f > avg ? cap : f;
+#else
     while ((double)f > avg && f > 0.0f) f = nextafterf(f, 0.0f);
     return f;
+#endif
 }
 template <typename T> __host__ __device__ __forceinline__ T tw_store(double t, double avg);
 template <> __host__ __device__ __forceinline__ float tw_store<float>(double t, double avg)

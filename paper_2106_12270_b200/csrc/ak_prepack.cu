@@ -48,6 +48,26 @@ template <typename T> __device__ __forceinline__ int item_class(T v, double avg)
     return d == avg ? 2 : (d < avg ? 0 : 1);  // 0 light, 1 heavy, 2 exactly full
 }
 
+// item_class in the weight type: for floats, (double)v < avg <=> v < ru(avg)
+// (no float lies strictly between rd(avg) and ru(avg)) and v == avg only
+// when avg is itself a float
+template <typename T> struct ClassCut {
+    T a;
+    bool exact;
+    __device__ explicit ClassCut(double avg) : a(T(0)), exact(true)
+    {
+#ifdef __CUDA_ARCH__
+        if constexpr (sizeof(T) == 4) {
+            a = __double2float_ru(avg);
+            exact = (double)a == avg;
+        } else {
+            a = avg;
+        }
+#endif
+    }
+    __device__ __forceinline__ int operator()(T v) const { return v < a ? 0 : (exact && v == a ? 2 : 1); }
+};
+
 // exclusive block scan of two counters (PP_TB threads)
 __device__ __forceinline__ void block_scan2(u32 a, u32 b, u32 &ea, u32 &eb, u32 &ta, u32 &tb)
 {
@@ -199,13 +219,14 @@ __global__ void __launch_bounds__(PP_TB) k_prepack_block(const T *__restrict__ w
         __syncthreads();
     }
     // count per (row, warp); exactly-full items are final at once
+    const ClassCut<T> cls(avg);
     u32 cw = 0;
     for (u32 r = 0; r < R; ++r) {
         const u32 i = r * PP_TB + threadIdx.x;
         int c = 3;
         if (i < len) {
             const T v = S.sw[i];
-            c = item_class(v, avg);
+            c = cls(v);
             if (c == 2) {
                 RowT row;
                 row.tw = (TwT)v;
@@ -237,7 +258,7 @@ __global__ void __launch_bounds__(PP_TB) k_prepack_block(const T *__restrict__ w
     // class-compacted terms (avg - w for lights, w - avg for heavies) and offsets
     for (u32 r = 0; r < R; ++r) {
         const u32 i = r * PP_TB + threadIdx.x;
-        const int c = i < len ? item_class(S.sw[i], avg) : 3;
+        const int c = i < len ? cls(S.sw[i]) : 3;
         const unsigned lb = __ballot_sync(0xffffffffu, c == 0), hb = __ballot_sync(0xffffffffu, c == 1);
         if (c < 2) {  // one store path for both classes (no divergence)
             const bool l = c == 0;
