@@ -191,16 +191,21 @@ def fast_section_reference(tw, al, avg, lo, span, seed, strm, ctr0, m):
     return O.rule(tw, al, avg, u, lo, span)
 
 
-@pytest.mark.parametrize("ctr0,dtype,S", [(0, torch.float32, 4096), (5, torch.float32, 4096),
-                                          (2**32 - 3, torch.float32, 4096), (7, torch.float64, 1 << 14),
-                                          (3, torch.float64, 4096)])
-def test_fast_rng_sectioned_bit_exact(ctr0, dtype, S):
+@pytest.mark.parametrize("ctr0,dtype,S,tail", [(0, torch.float32, 4096, 1000), (5, torch.float32, 4096, 1000),
+                                               (2**32 - 3, torch.float32, 4096, 1000),
+                                               (7, torch.float64, 1 << 14, 1000),
+                                               (3, torch.float64, 4096, 1000),
+                                               (1, torch.float32, 3000, 7),      # non-power-of-two sections
+                                               (2, torch.float32, 4096, 2),      # a 2-row last section
+                                               (4, torch.float64, 2048, 1)])     # a 1-row last section
+def test_fast_rng_sectioned_bit_exact(ctr0, dtype, S, tail):
     """rng="philox4x32": the sectioned kernel (interior fast path, checked
     edges, misaligned outputs, several passes per call; f64 rows staged as
     rows (S=4096) or, for 2^14-row sections, as threshold/alias arrays)
     against a numpy restatement of the GPU-native stream."""
     g = np.random.default_rng(ctr0 + 1)
-    n, M = 3 * S + 1000, 1_500_003
+    # enough draws that even a 1- or 2-row last section runs whole CTA steps
+    n, M = 3 * S + tail, (1_500_003 if tail >= 1000 else 15_000_007)
     w = (g.random(n) + 1e-3).astype(np.float32 if dtype == torch.float32 else np.float64)
     ws = ak.make_weight_set(torch.from_numpy(w).to(DEV))
     t = ak.psa_construct(ws)
