@@ -84,7 +84,7 @@ def test_golden_prepack(golden):
                            rtol=0, atol=1e-9 * ws.average)
 
 
-@pytest.mark.parametrize("bs,thr", [(2, 1), (7, 2), (64, 4), (4096, 8), (1000, 300)])
+@pytest.mark.parametrize("bs,thr", [(2, 1), (7, 2), (64, 4), (4096, 8), (1000, 300), (11000, 8)])
 def test_random_prepack_vs_oracle(rng, bs, thr):
     for trial in range(10):
         n = int(np.exp(rng.uniform(0, np.log(200_000)))) + 1
