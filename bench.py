@@ -320,6 +320,13 @@ def run_ours(a):
     build_bytes = N * (2 * b_w + b_row)
     # reference-RNG (bit-exact mode) throughput of the same pass, for context
     t_pass_ref = time_launch(lambda: sectioned_sample_into(table, S_eff, counts_d, offs_d, f0, c0, r0, out, o0, "reference"))
+    # PSA+ (block prepack + residual PSA) on the same weights,
+    # as a public-API call (it reads two counts back to the host), for context
+    # (best of 5: the call waits on the host twice, so a descheduled host
+    # thread shows up as idle device time)
+    ak.psa_plus_construct(ws)
+    t_plus = min(time_launch(lambda: ak.psa_plus_construct(ws), reps=1) for _ in range(5))
+    torch.cuda.empty_cache()
 
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -446,6 +453,8 @@ def run_ours(a):
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak, "traffic": traffic, "kernel": "k_sample_sectioned",
                          "algorithmic_bytes_per_launch": pass_bytes, "peak_kind": peak_kind},
+            "build_psa_plus": {"items_per_s": N / t_plus, "ms": t_plus * 1e3,
+                               "frac": build_bytes / t_plus / 1e9 / peak},
             "sampling_reference_rng": {"samples_per_s": d0 / t_pass_ref,
                                        "frac": pass_bytes / t_pass_ref / 1e9 / peak},
             "e2e": e2e,

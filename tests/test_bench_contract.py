@@ -35,7 +35,7 @@ def test_our_arm_contract():
     d = run(["--steps", "1", "--warmup", "1", "--n", "1e6", "--samples", "1e8", "--no-cpu",
              "--e2e-samples", "1e7", "--e2e-steps", "1"], 600)
     assert KEYS <= set(d)
-    for k in ("roofline", "clocks", "gpu_launches", "build"):
+    for k in ("roofline", "clocks", "gpu_launches", "build", "build_psa_plus"):
         assert k in d
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5
