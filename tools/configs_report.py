@@ -7,7 +7,9 @@ C1  N=1e6 uniform f64: PSA construction + 1e6 naive samples
 C2  N=1e8 uniform f32: construction + 1e9 naive samples
 C3  N=1e8 shuffled power law (alpha=1) f32 (and f64): construction
 C4  N=1e9 f32 table: one pass of batched/sectioned sampling (the bench's)
-C5  N=1e9 uniform f64 (and f32): construction
+C5  N=1e9 uniform f64 (and f32): construction; make_weight_set and PSA+
+Component operators of the reference API (partition_items, compute_split_plan,
+pack_all, partial_pary_search) on the C2 weights.
 Algorithmic bytes (SURVEY.md §8d): build N(2 b_w + b_row); naive M(b_row + 8);
 sectioned M*8 + rows of the sections drawn.
 """
@@ -106,6 +108,47 @@ def main():
                         frac=byts / s / 1e9 / PEAK, parity="bit-exact (reference rng) vs oracle: tests"))
     del ws, t, o
     ws, t = build_row("C5", 10**9, "uniform", torch.float64, out)
+    del t
+    # C5 weights: make_weight_set and PSA+ (f64 here; f32 below)
+    for dt in (torch.float64, torch.float32):
+        wsd = ws if dt == torch.float64 else ak.make_weight_set(ws.weights.float())
+        bw = 8 if dt == torch.float64 else 4
+        s = timed(lambda: ak.make_weight_set(wsd.weights), reps=5)
+        out.append(dict(config="C5", op=f"make_weight_set N=1e9 {str(dt)[6:]}", seconds=s, rate=10**9 / s,
+                        rate_unit="items/s", gbs=10**9 * bw / s / 1e9, frac=10**9 * bw / s / 1e9 / PEAK,
+                        parity="total bit-identical to np.sum: tests/test_gpu_core.py"))
+        s = min(timed(lambda: ak.psa_plus_construct(wsd), reps=1) for _ in range(5))
+        byts = 10**9 * (3 * bw + 4)
+        out.append(dict(config="C5", op=f"psa_plus_construct N=1e9 {str(dt)[6:]} (block 4096)", seconds=s,
+                        rate=10**9 / s, rate_unit="items/s", gbs=byts / s / 1e9, frac=byts / s / 1e9 / PEAK,
+                        parity="oracle PSA+ composition: tests/test_gpu_prepack.py"))
+        del wsd
+    del ws
+    # the reference's component operators on C2 weights (API parity layer;
+    # the fused builder above does not use them)
+    ws = weights(10**8, "uniform", torch.float32)
+    s = timed(lambda: ak.partition_items(ws), reps=3)
+    byts = 10**8 * (4 + 12 + 8)  # read w; write (index, weight) and one prefix per item
+    out.append(dict(config="C2", op="partition_items N=1e8 f32", seconds=s, rate=10**8 / s, rate_unit="items/s",
+                    gbs=byts / s / 1e9, frac=byts / s / 1e9 / PEAK, parity="exact order / prefixes: tests"))
+    part = ak.partition_items(ws)
+    nsec = 10**8 // 2048
+    s = timed(lambda: ak.compute_split_plan(part, nsec), reps=3)
+    out.append(dict(config="C2", op=f"compute_split_plan s={nsec}", seconds=s, rate=nsec / s,
+                    rate_unit="bounds/s", gbs=0.0, frac=0.0, parity="bit-identical to the reference: tests"))
+    plan = ak.compute_split_plan(part, nsec)
+    tab = ak.AliasTable.empty(10**8, ws.total, torch.float32, ws.weights.device)
+    from paper_2106_12270_b200.pack import pack_all
+    s = timed(lambda: pack_all(part, plan, tab), reps=3)
+    byts = 10**8 * (12 + 8 + 8)
+    out.append(dict(config="C2", op=f"pack_all (reference sweep) s={nsec}", seconds=s, rate=10**8 / s,
+                    rate_unit="items/s", gbs=byts / s / 1e9, frac=byts / s / 1e9 / PEAK,
+                    parity="bit-identical to the reference sweep: tests"))
+    hay = part.lprefix
+    q = torch.sort(torch.rand(10**6, dtype=torch.float64, device=hay.device) * float(hay[-1]))[0]
+    s = timed(lambda: ak.partial_pary_search(hay, q, 32), reps=3)
+    out.append(dict(config="C2", op=f"partial_pary_search hay={hay.numel():.1e} q=1e6 p=32", seconds=s,
+                    rate=10**6 / s, rate_unit="queries/s", gbs=0.0, frac=0.0, parity="= searchsorted: tests"))
     for r in out:
         print(f"{r['config']:3s} {r['op']:55s} {r['seconds'] * 1e3:9.3f} ms  {r['rate']:.3e} {r['rate_unit']:9s} "
               f"{r['gbs']:7.0f} GB/s  {100 * r['frac']:5.1f}%  {r['parity']}")
