@@ -56,7 +56,7 @@ constexpr int VV = 8;              // items per lane
 constexpr int CH = 32 * VV;        // items per chunk (one warp)
 constexpr int NW = TB / 32;        // chunks per tile
 constexpr int TILE = TB * VV;      // items per tile
-constexpr int SUPER = 32;          // tiles per pass-1 CTA (look-back granularity)
+constexpr int SUPER = 32;          // max tiles per pass-1 CTA (look-back granularity)
 constexpr u64 NONE64 = ~0ull;
 constexpr unsigned char NOFH = 0xFF;
 
@@ -65,6 +65,7 @@ constexpr unsigned char NOFH = 0xFF;
 // ---------------------------------------------------------------------------
 struct BuildWs {
     u64 nt, nst;  // tiles, super-tiles
+    u32 super;    // tiles per super-tile (SUPER, fewer for small n: enough scan CTAs)
     unsigned int *counter;
     u32 *status;            // [nst] 0 none, 1 aggregate, 2 inclusive
     dd *agg_D, *agg_H;      // [nst] super-tile aggregates (write once)
@@ -83,10 +84,18 @@ struct BuildWs {
 
 __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// tiles per scan CTA: 32, or as few as 4 (one per warp) so that small
+// inputs still spread over ~2 CTAs per SM
+inline u32 super_for(u64 nt)
+{
+    const u64 s = nt / 296;
+    return (u32)(s >= SUPER ? SUPER : (s < 4 ? 4 : s & ~3ull));
+}
+
 template <typename F> inline void layout(u64 n, F &&take)
 {
     u64 nt = (n + TILE - 1) / TILE;
-    u64 nst = (nt + SUPER - 1) / SUPER;
+    u64 nst = (nt + super_for(nt) - 1) / super_for(nt);
     size_t sizes[19] = {256,          nst * 4,      nst * 16,       nst * 16,       nst * 8,
                         nst * 16,     nst * 16,     nst * 8,        (nt + 1) * 16,  (nt + 1) * 16,
                         (nt + 1) * 8, nt * 8,       nt * NW * 8,    nt * NW * 8,    nt * NW,
@@ -98,7 +107,8 @@ inline BuildWs carve(void *ws, u64 n)
 {
     BuildWs W;
     W.nt = (n + TILE - 1) / TILE;
-    W.nst = (W.nt + SUPER - 1) / SUPER;
+    W.super = super_for(W.nt);
+    W.nst = (W.nt + W.super - 1) / W.super;
     char *base = (char *)ws;
     size_t off = 0;
     char *p[19];
@@ -332,8 +342,8 @@ __global__ void __launch_bounds__(SC_WARPS * 32) k_build_scan(const T *__restric
     }
     __syncthreads();
     const u64 st = s_st;
-    const u64 t0 = st * SUPER;
-    const u64 tn = (t0 + SUPER <= W.nt) ? SUPER : W.nt - t0;
+    const u64 t0 = st * W.super;
+    const u64 tn = (t0 + W.super <= W.nt) ? W.super : W.nt - t0;
     T *ring = reinterpret_cast<T *>(scan_smem) + (size_t)wid * NW * CH;
     const T avgT = avg_floor<T>(avg);
     auto full_chunk = [&](u64 g) { return (g + 1) * CH <= n; };
