@@ -11,6 +11,9 @@
 // construction path is the fused builder in ak_build.cu.
 #include "ak_common.cuh"
 
+#include <mutex>
+#include <unordered_map>
+
 namespace {
 
 constexpr int PT_THREADS = 256;
@@ -709,27 +712,39 @@ int ak_partial_pary_search(const double *hay, uint64_t n, const double *q, uint6
 {
     cudaStream_t st = ak_stream(stream);
     if (p < 3) return AK_ERR_VALUE;
+    // 64 bytes of per-device scratch (sortedness flags, the contracted
+    // range), allocated once: no allocation on the call path
+    static std::mutex mu;
+    static std::unordered_map<int, int *> scratch;
+    int dev = 0;
+    AK_CUDA_TRY(cudaGetDevice(&dev));
     int *flag = nullptr;
-    i64 *ab = nullptr;
-    AK_CUDA_TRY(cudaMallocAsync((void **)&flag, 64, st));
-    ab = (i64 *)((char *)flag + 16);
-    AK_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), st));
-    if (n > 1) k_check_sorted<<<64, 256, 0, st>>>(hay, n, flag);
-    int f1 = 0, f2 = 0;
-    AK_CUDA_TRY(cudaMemcpyAsync(&f1, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-    AK_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), st));
-    if (m > 1) k_check_sorted<<<64, 256, 0, st>>>(q, m, flag);
-    AK_CUDA_TRY(cudaMemcpyAsync(&f2, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = scratch.find(dev);
+        if (it == scratch.end()) {
+            AK_CUDA_TRY(cudaMalloc((void **)&flag, 64));
+            scratch[dev] = flag;
+        } else {
+            flag = it->second;
+        }
+    }
+    i64 *ab = (i64 *)((char *)flag + 16);
+    AK_CUDA_TRY(cudaMemsetAsync(flag, 0, 2 * sizeof(int), st));
+    const unsigned g = (unsigned)ak_num_sms() * 8;
+    if (n > 1) k_check_sorted<<<g, 256, 0, st>>>(hay, n, flag);
+    if (m > 1) k_check_sorted<<<g, 256, 0, st>>>(q, m, flag + 1);
+    int f[2] = {0, 0};
+    AK_CUDA_TRY(cudaMemcpyAsync(f, flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
     AK_CUDA_TRY(cudaStreamSynchronize(st));
     AK_LAUNCH_CHECK("k_check_sorted");
     int rc = AK_OK;
-    if (f1 || f2) rc = AK_ERR_UNSORTED_INPUT;
+    if (f[0] || f[1]) rc = AK_ERR_UNSORTED_INPUT;
     else if (m > 0) {
         k_contract<<<1, 32, 0, st>>>(hay, n, q, m, (int)p, ab);
         k_lower_bound<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(hay, q, m, ab, out);
         rc = ak_check_launch("k_lower_bound");
     }
-    cudaFreeAsync(flag, st);
     return rc;
 }
 
