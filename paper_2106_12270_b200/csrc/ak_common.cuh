@@ -40,6 +40,7 @@ int ak_check_launch(const char *where);
 static inline cudaStream_t ak_stream(void *s) { return (cudaStream_t)s; }
 
 int ak_num_sms();
+void *ak_stream_scratch(cudaStream_t st);  // 256 B per (device, stream), never freed
 
 // ---------------------------------------------------------------------------
 // table rows

@@ -8,6 +8,9 @@
 // is not bit-identical to glibc's, so bit-exact counts need the host libm.
 // This file is compiled with -ffp-contract=off (CPython never fuses mul+add).
 // 61,036 nodes at N=1e9, S=2^14 take well under a millisecond here.
+#include <utility>
+#include <map>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include <cfenv>
@@ -37,6 +40,26 @@ int ak_check_launch(const char *where)
         return AK_ERR_CUDA;
     }
     return AK_OK;
+}
+
+// 256 bytes of device scratch per (device, stream) for the small status
+// words the entry points read back (flags, counts): allocated once, so no
+// allocation sits on a call path; per stream, so concurrent calls on
+// different streams never share it.
+void *ak_stream_scratch(cudaStream_t st)
+{
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, void *> bufs;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> g(mu);
+    auto key = std::make_pair(dev, st);
+    auto it = bufs.find(key);
+    if (it != bufs.end()) return it->second;
+    void *p = nullptr;
+    if (cudaMalloc(&p, 256) != cudaSuccess) return nullptr;
+    bufs[key] = p;
+    return p;
 }
 
 int ak_num_sms()

@@ -11,9 +11,6 @@
 // construction path is the fused builder in ak_build.cu.
 #include "ak_common.cuh"
 
-#include <mutex>
-#include <unordered_map>
-
 namespace {
 
 constexpr int PT_THREADS = 256;
@@ -712,23 +709,8 @@ int ak_partial_pary_search(const double *hay, uint64_t n, const double *q, uint6
 {
     cudaStream_t st = ak_stream(stream);
     if (p < 3) return AK_ERR_VALUE;
-    // 64 bytes of per-device scratch (sortedness flags, the contracted
-    // range), allocated once: no allocation on the call path
-    static std::mutex mu;
-    static std::unordered_map<int, int *> scratch;
-    int dev = 0;
-    AK_CUDA_TRY(cudaGetDevice(&dev));
-    int *flag = nullptr;
-    {
-        std::lock_guard<std::mutex> g(mu);
-        auto it = scratch.find(dev);
-        if (it == scratch.end()) {
-            AK_CUDA_TRY(cudaMalloc((void **)&flag, 64));
-            scratch[dev] = flag;
-        } else {
-            flag = it->second;
-        }
-    }
+    int *flag = (int *)ak_stream_scratch(st);
+    if (!flag) return AK_ERR_CUDA;
     i64 *ab = (i64 *)((char *)flag + 16);
     AK_CUDA_TRY(cudaMemsetAsync(flag, 0, 2 * sizeof(int), st));
     const unsigned g = (unsigned)ak_num_sms() * 8;

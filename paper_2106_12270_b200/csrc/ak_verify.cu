@@ -184,15 +184,14 @@ int ak_frequency_counts(const int64_t *samples, uint64_t m, uint64_t n, int64_t 
 {
     cudaStream_t st = ak_stream(stream);
     if (n < 1) return AK_ERR_VALUE;
-    int *oor = nullptr;
-    AK_CUDA_TRY(cudaMallocAsync((void **)&oor, 16, st));
+    int *oor = (int *)ak_stream_scratch(st);
+    if (!oor) return AK_ERR_CUDA;
     AK_CUDA_TRY(cudaMemsetAsync(oor, 0, 16, st));
     AK_CUDA_TRY(cudaMemsetAsync(counts, 0, n * sizeof(int64_t), st));
     if (m) k_freq<<<grid_of(m), 256, 0, st>>>(samples, m, n, (unsigned long long *)counts, oor);
     int f = 0;
     AK_CUDA_TRY(cudaMemcpyAsync(&f, oor, sizeof(int), cudaMemcpyDeviceToHost, st));
     AK_CUDA_TRY(cudaStreamSynchronize(st));
-    cudaFreeAsync(oor, st);
     AK_LAUNCH_CHECK("k_freq");
     return f ? AK_ERR_INDEX_OUT_OF_RANGE : AK_OK;
 }
@@ -224,8 +223,8 @@ int ak_soa_to_rows(const double *tw, const int64_t *alias, uint64_t n, int dtype
 int ak_count_unwritten(const void *rows, int dtype, uint64_t n, uint64_t *unwritten, void *stream)
 {
     cudaStream_t st = ak_stream(stream);
-    unsigned long long *c = nullptr;
-    AK_CUDA_TRY(cudaMallocAsync((void **)&c, 16, st));
+    unsigned long long *c = (unsigned long long *)ak_stream_scratch(st);
+    if (!c) return AK_ERR_CUDA;
     AK_CUDA_TRY(cudaMemsetAsync(c, 0, 16, st));
     if (n) {
         if (dtype == AK_F32) k_unwritten<RowF32><<<grid_of(n), 256, 0, st>>>((const RowF32 *)rows, n, c);
@@ -234,7 +233,6 @@ int ak_count_unwritten(const void *rows, int dtype, uint64_t n, uint64_t *unwrit
     unsigned long long h = 0;
     AK_CUDA_TRY(cudaMemcpyAsync(&h, c, sizeof(h), cudaMemcpyDeviceToHost, st));
     AK_CUDA_TRY(cudaStreamSynchronize(st));
-    cudaFreeAsync(c, st);
     AK_LAUNCH_CHECK("k_unwritten");
     *unwritten = h;
     return AK_OK;
