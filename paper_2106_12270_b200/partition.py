@@ -85,10 +85,11 @@ def partition_items(w: WeightSet) -> LightHeavyPartition:
                                   _lib.ptr(ws), ws.numel(), _lib.stream_ptr(dev)),
                    "partition_items")
     a, b = int(nl.value), int(nh.value)
+    # exact-length views of the n-sized outputs (no copies; the unused tails
+    # stay allocated with them)
     return LightHeavyPartition(
-        l_index=l_idx[:a].clone(), l_weight=l_w[:a].clone(), h_index=h_idx[:b].clone(),
-        h_weight=h_w[:b].clone(), lprefix=lpre[: a + 1].clone(), hprefix=hpre[: b + 1].clone(),
-        avg=w.average,
+        l_index=l_idx[:a], l_weight=l_w[:a], h_index=h_idx[:b], h_weight=h_w[:b],
+        lprefix=lpre[: a + 1], hprefix=hpre[: b + 1], avg=w.average,
     )
 
 
