@@ -162,6 +162,41 @@ def test_frequency_counts_device():
     assert ak.frequency_counts(torch.empty(0, dtype=torch.int64, device=DEV), 2).tolist() == [0, 0]
 
 
+def test_status_words_per_stream_threads():
+    """Entry points that read a status word back (frequency_counts,
+    count_unwritten, partial_pary_search) keep one scratch per (device,
+    stream): calls from several host threads on their own streams, one of
+    them failing, must not see each other's flags."""
+    import threading
+
+    bad = torch.tensor([0, 1], device=DEV)
+    good = torch.tensor([1, 2, 2], device=DEV)
+    hay = torch.arange(1000, dtype=torch.float64, device=DEV)
+    errs = []
+
+    def worker(k):
+        s = torch.cuda.Stream()
+        try:
+            with torch.cuda.stream(s):
+                for it in range(30):
+                    if (k + it) % 2:
+                        with pytest.raises(ak.IndexOutOfRange):
+                            ak.frequency_counts(bad, 3)
+                    else:
+                        assert ak.frequency_counts(good, 3).tolist() == [1, 2, 0]
+                    q = torch.tensor([3.5, 10.0, 999.0], dtype=torch.float64, device=DEV)
+                    assert ak.partial_pary_search(hay, q, 8).tolist() == [4, 10, 999]
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+
+
 def philox4x32_words(call: np.ndarray, strm: int, seed: int):
     """numpy Philox4x32-10 (Random123 constants) of counters (call lo, call
     hi, strm lo, strm hi) under key (seed lo, seed hi): the two 64-bit words
