@@ -613,7 +613,7 @@ __device__ __forceinline__ u32 warp_excl_count(u32 cnt, u32 &total, int lane)
 // pass-1 chunk bounds (8 lanes at once), the count inside the chunk from its
 // canonical keys.  Outputs: the boundary's heavy rank, the chunk holding that
 // rank, and the item of that heavy (the first heavy past the boundary).
-constexpr int HCAP = 1472;       // heavies per merge round (shared memory for 4 CTAs per SM)
+constexpr int HCAP = 1300;       // heavies per merge round (shared memory for 5 CTAs per SM)
 
 struct SplitOut {
     u64 *hrank;   // [nt+2]
@@ -750,11 +750,10 @@ struct SecSmem {
     u64 LK[TILE + 2];              // own light keys (own frame, encoded), rank order; ~0 sentinel
     u64 HK[HCAP + 1];              // heavy keys (own frame, encoded); ~0 sentinel
     u32 HI[HCAP + 1];              // heavy items; ~0 sentinel (LS = HI + 1 = 0: unresolved)
-    u64 SK[HCAP];                  // heavy -> encoded key of its successor light (~0: none
-                                   // here); before the merge: the heavy's key in its chunk
-                                   // frame (a double)
+                                   // (HK holds the tile-frame key bits between the rebuild and
+                                   // the conversion; a slot's chunk is its item's chunk)
+    unsigned short SR[HCAP];       // heavy -> rank of its successor light (nL: none here)
     dd Dwin[32];                   // frame offset (chunk's tile base - own base) per window chunk
-    unsigned char CI[HCAP];        // window chunk of each heavy slot
     u32 lfirst;
     u64 next_item;                 // item of the heavy ranked jend (first of the next round)
 };
@@ -792,7 +791,7 @@ __device__ __forceinline__ void chunk_ranks(const BuildWs &W, u64 n, u64 g0, int
 }
 
 template <typename T>
-__global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u64 n, double avg,
+__global__ void __launch_bounds__(TB, 5) k_build_pack(const T *__restrict__ w, u64 n, double avg,
                                                       BuildWs W, SplitOut O,
                                                       typename RowOf<T>::type *__restrict__ rows)
 {
@@ -885,9 +884,8 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
             for (int q = 0; q < VV; ++q) {
                 const int sl = r0 + __popc(m & ((1u << q) - 1));
                 if (((m >> q) & 1) && sl >= 0 && sl < (int)nH) {
-                    P.SK[sl] = (u64)__double_as_longlong(k[q]);
+                    P.HK[sl] = (u64)__double_as_longlong(k[q]);  // tile frame until converted
                     P.HI[sl] = item0 + q;
-                    P.CI[sl] = (unsigned char)ci;
                 }
             }
             const int want = (int)nH - r0;  // this lane holds rank jend?
@@ -900,7 +898,8 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
         __syncthreads();
         // heavy keys into the own frame (double-double), one thread per heavy
         for (u32 j = threadIdx.x; j < nH; j += TB)
-            P.HK[j] = key_enc_dd(add_dd_d(P.Dwin[P.CI[j]], __longlong_as_double((long long)P.SK[j])));
+            P.HK[j] = key_enc_dd(add_dd_d(P.Dwin[(u32)(P.HI[j] / CH - gcur)],
+                                          __longlong_as_double((long long)P.HK[j])));
         if (!last_round && wid == 0 && P.next_item == NONE64) {
             // rank jend lies past the enumerated chunks
             const u64 gl = gcur + 31;
@@ -961,7 +960,7 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
                 u64 hk = P.HK[j];
                 for (u32 d = 0; d < steps; ++d) {
                     if (hk <= lk) {
-                        P.SK[j] = lk;
+                        P.SR[j] = (unsigned short)(lfirst + i);
                         ++j;
                         hk = P.HK[j];
                     } else {
@@ -977,8 +976,8 @@ __global__ void __launch_bounds__(TB, 4) k_build_pack(const T *__restrict__ w, u
         const u64 nxt = last_round ? after : P.next_item;
         for (u32 j = threadIdx.x; j < nH; j += TB) {
             const u32 item = P.HI[j];
-            const u64 sk = P.SK[j];
-            const double DL = sk != KEY_INF ? key_dec(sk) : secbound;
+            const u32 sr = P.SR[j];
+            const double DL = sr < nL ? key_dec(P.LK[sr]) : secbound;
             const double tw = (key_dec(P.HK[j]) - DL) + avg;
             u64 al;
             if (j + 1 < nH) al = (u64)P.HI[j + 1] + 1;
