@@ -156,6 +156,24 @@ def test_f32_tables(rng):
         assert rep.ok, rep
 
 
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_many_heavies_per_section(rng, dtype):
+    """Few light items with deep deficits among many barely-heavy items: a
+    light tile's sections then cover ~1800 heavies, more than one merge round
+    (HCAP) holds, so the multi-round path of the pack runs."""
+    n = 300_000
+    light = rng.random(n) < 0.1
+    w = np.where(light, 1e-3 * (1 + rng.random(n)), 1.1 + 0.01 * rng.random(n))
+    if dtype == torch.float32:
+        w = w.astype(np.float32)
+    ws = ak.make_weight_set(torch.from_numpy(np.ascontiguousarray(w)).to(DEV))
+    w64 = ws.weights.double().cpu().numpy()
+    am, _, gap = compare(ak.psa_construct(ws), w64, ws.total)
+    assert am == 0
+    assert gap <= (1e-9 if dtype == torch.float64 else 1e-6)
+    assert ak.validate_table(ak.psa_construct(ws), ws, tol=1e-9 if dtype == torch.float64 else 1e-4).ok
+
+
 def test_vose_api_and_args():
     ws = ak.make_weight_set([1.0, 5.0])
     assert ak.validate_table(ak.psa_construct(ws, s=64), ws).ok
