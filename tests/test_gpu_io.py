@@ -62,3 +62,17 @@ def test_corrupt_files_rejected(tmp_path):
     q.write_bytes(b"WTS1" + struct.pack("<Q", 3) + b"\0" * 8)
     with pytest.raises(FormatError):
         ak.load_weights(q)
+
+
+def test_bench_rows_on_device():
+    """aliaskit.bench-schema rows measured on the device (bench.py:135-203)."""
+    from paper_2106_12270_b200.bench import BenchConfig, bench_run, rows_to_csv
+    cfg = BenchConfig(n=20_000, methods=("vose", "psa", "psa-plus"), samplers=("baseline", "sectioned"),
+                      samples=50_000, section_size=1024, repetitions=5, warmup=1)
+    rows = bench_run(cfg)
+    assert len(rows) == 5 * 6
+    med = [r for r in rows if r["repetition"] == "median"]
+    assert [r["method"] for r in med] == ["vose", "psa", "psa-plus", "baseline", "sectioned"]
+    assert all(r["throughput_per_s"] > 0 and "backend=b200" in r["param"] for r in rows)
+    assert [r["s"] for r in med] == [1, 64, 64, 0, 1024]
+    assert rows_to_csv(rows).count("\n") == len(rows) + 1

@@ -119,3 +119,33 @@ def test_chi_square_matches_reference(reference):
             continue
         obs = rng.multinomial(int(rng.integers(10, 10**6)), probs)
         assert chi_square_test(obs, probs) == reference.chi_square_test(obs, probs)
+
+
+# ---- CSV bench rows (aliaskit.bench schema) -------------------------------
+
+def test_bench_config_validation_mirrors_reference():
+    from paper_2106_12270_b200.bench import BenchConfig, ConfigError
+    cases = [
+        (dict(n=0, methods=("psa",)), "n must be at least 1"),
+        (dict(dist="zipf", methods=("psa",)), "unknown distribution"),
+        (dict(methods=("alias",)), "unknown method"),
+        (dict(samplers=("fast",)), "unknown sampler"),
+        (dict(), "nothing to benchmark"),
+        (dict(methods=("psa",), repetitions=4), "at least 5 repetitions"),
+        (dict(methods=("psa",), warmup=-1), "warmup"),
+        (dict(methods=("psa",), splits=0), "splits and workers"),
+        (dict(samplers=("baseline",), samples=0), "samples and section_size"),
+        (dict(methods=("psa",), chunk_capacity=1), "chunk_capacity"),
+    ]
+    for kw, msg in cases:
+        with pytest.raises(ConfigError, match=msg):
+            BenchConfig(**kw).validate()
+    BenchConfig(methods=("vose", "psa", "psa-plus"), samplers=("baseline", "sectioned")).validate()
+
+
+def test_rows_to_csv_schema():
+    from paper_2106_12270_b200.bench import CSV_HEADER, _rows, rows_to_csv
+    rows = _rows("psa", 10, 64, 1, {"dist": "uniform", "seed": 1, "backend": "b200"}, [10, 30, 20, 40, 50], 10)
+    csv = rows_to_csv(rows).splitlines()
+    assert csv[0] == CSV_HEADER == "method,n,s,workers,param,repetition,wall_time_ns,throughput_per_s"
+    assert len(csv) == 7 and csv[-1].startswith("psa,10,64,1,dist=uniform;seed=1;backend=b200,median,30,")
