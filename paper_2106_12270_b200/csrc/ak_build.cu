@@ -30,7 +30,8 @@
 //                    (reduce-scatter), light counts, first heavies, the
 //                    light bitmask, the tile's monotone chunk bounds; a
 //                    single-pass decoupled look-back over super-tiles (32
-//                    tiles per CTA) produces the exclusive tile bases DLb[t],
+//                    tiles per CTA; 4-32 for small inputs, so at least ~2
+//                    CTAs per SM) produces the exclusive tile bases DLb[t],
 //                    DHb[t] (double-double sums) and light counts kL[t].
 //  2. k_build_coarse merge of the two tile-boundary sequences: for each tile
 //                    the first heavy tile covering its light keys (T1) and
@@ -44,9 +45,11 @@
 //                    lights' neighbours in key space) are merged once by a
 //                    merge path over order-preserving 64-bit integer keys in
 //                    shared memory; each row is written exactly once (light
-//                    rows by consecutive threads, coalesced).
+//                    rows by consecutive threads, coalesced).  43 KB of shared
+//                    memory and 48 registers: 5 CTAs per SM (the pack is
+//                    occupancy bound: 3/4/5 per SM = 14.3/12.6/11.6 ms at 1e9).
 //  DRAM traffic ~ read w twice + write the rows once = the algorithmic bytes
-//  (ncu: profiles/r1c_ncu_bench_pass.json).
+//  (ncu: profiles/r1k_ncu_bench_pass.json).
 #include "ak_common.cuh"
 
 namespace {

@@ -4,10 +4,12 @@
 //   ak_sample_naive        _fill_samples over the whole table (sample.py:73-84)
 //   ak_sample_from_uniforms  the bucket rule fed explicit uniforms
 //   ak_sample_sectioned    sectioned_sample (sample.py:243-267): one CTA per
-//                          section (persistent, grid = SMs), the section's rows
-//                          staged in shared memory by a bulk async copy
-//                          (cp.async.bulk + mbarrier), every draw served from
-//                          shared memory.
+//                          SM, each a balanced slice of the pass's draw space;
+//                          a section's rows staged in shared memory by a bulk
+//                          async copy (cp.async.bulk + mbarrier), every draw
+//                          served from shared memory; the fast-RNG interior
+//                          keeps three Philox calls in flight per thread with
+//                          the round keys in the constant bank.
 //
 // Draws use Philox2x64-10 word 0 (AK_RNG_REFERENCE, bit-exact with the
 // reference) or the GPU-native Philox4x32-10 (AK_RNG_PHILOX4X32: one call
