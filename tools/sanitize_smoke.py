@@ -13,13 +13,16 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2106_12270_b200 as ak  # noqa: E402
 
 g = np.random.default_rng(11)
-for n, kind in ((1, 0), (7, 0), (2049, 1), (70_001, 0), (70_001, 2)):
+for n, kind in ((1, 0), (7, 0), (2049, 1), (70_001, 0), (70_001, 2), (60_000, 3)):
     if kind == 0:
         w = g.random(n) + 1e-6
     elif kind == 1:
         w = g.pareto(1.1, n) + 1e-6
-    else:
+    elif kind == 2:
         w = np.floor(g.random(n) * 5) + 1.0
+    else:  # few deep lights among many barely-heavy items: multi-round pack sections
+        light = g.random(n) < 0.1
+        w = np.where(light, 1e-3 * (1 + g.random(n)), 1.1 + 0.01 * g.random(n))
     for dt in (torch.float64, torch.float32):
         ws = ak.make_weight_set(torch.from_numpy(w.astype(np.float32) if dt == torch.float32 else w).cuda())
         t = ak.psa_construct(ws)
@@ -34,5 +37,11 @@ for n, kind in ((1, 0), (7, 0), (2049, 1), (70_001, 0), (70_001, 2)):
         z = ak.sectioned_sample(t, 64, 5000, ak.RngStream(3, 2), rng="reference")
         ak.validate_table(t, ws)
         ak.frequency_counts(x, n)
+        tq = ak.psa_plus_construct(ws)  # default block 4096 (bulk-copy staging when aligned)
+        assert tq.count_unwritten() == 0
+        ak.make_weight_set(ws.weights)
+        if n > 1:
+            hay = torch.sort(ws.weights.double())[0]
+            ak.partial_pary_search(hay, hay[:: max(1, n // 100)].contiguous(), 8)
 torch.cuda.synchronize()
 print("sanitize smoke ok")
