@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=float, default=1e9)
-    ap.add_argument("--samples", type=float, default=1e11, help="draws per step, whole job")
+    ap.add_argument("--samples", type=float, default=1e11, help="draws per step per GPU (weak scaling)")
     ap.add_argument("--section", type=int, default=1 << 14)
     ap.add_argument("--rng", default="philox4x32", choices=["philox4x32", "reference"])
     ap.add_argument("--dtype", default="float32", choices=["float32", "float64"])
