@@ -140,6 +140,8 @@ size_t ak_build_workspace_bytes(uint64_t n, int dtype);
  * double-double accurate.  `total` is WeightSet.total.  `rows` gets the
  * table in the layout of `dtype`.  Asynchronous; stats (nl, nh, tiles) are
  * readable afterwards with ak_build_stats. */
+/* Limit: n < 2^32 - 1 for both dtypes (u32 aliases in f32 rows, u32 item ids
+ * in the pack's merge windows); larger n returns AK_ERR_VALUE. */
 int ak_build_psa(const void *w, int dtype, uint64_t n, double total, void *rows, void *ws,
                  size_t ws_bytes, void *stream);
 /* ak_build_psa with the bucket size avg given instead of total/n (the PSA+
