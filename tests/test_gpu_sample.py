@@ -226,6 +226,21 @@ def fast_section_reference(tw, al, avg, lo, span, seed, strm, ctr0, m):
     return O.rule(tw, al, avg, u, lo, span)
 
 
+@pytest.mark.parametrize("ctr0,m", [(0, 1), (0, 100_001), (7, 100_000), (2**33 + 3, 54_321)])
+def test_fast_rng_naive_bit_exact(ctr0, m):
+    """rng="philox4x32" naive draws: draw i takes word (ctr0+i)&1 of the call
+    (ctr0+i)>>1 on the caller's stream, the rule over the whole table."""
+    g = np.random.default_rng(m)
+    w = g.random(5000) + 1e-3
+    ws = ak.make_weight_set(w)
+    t = ak.psa_construct(ws)
+    tw, al = t.to_numpy()
+    seed, stream = 0xABCDEF, 5
+    want = fast_section_reference(tw, al, t.average, 0, t.n, seed, stream, ctr0, m)
+    got = ak.sample_batch(t, m, ak.RngStream(seed, stream, ctr0), rng="philox4x32")
+    assert np.array_equal(got.cpu().numpy(), want)
+
+
 @pytest.mark.parametrize("ctr0,dtype,S,tail", [(0, torch.float32, 4096, 1000), (5, torch.float32, 4096, 1000),
                                                (2**32 - 3, torch.float32, 4096, 1000),
                                                (7, torch.float64, 1 << 14, 1000),
