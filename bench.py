@@ -205,7 +205,7 @@ def run_ours(a):
     S = a.section
     dtype = torch.float32 if a.dtype == "float32" else torch.float64
     b_w = 4 if dtype == torch.float32 else 8
-    b_row = b_w + 4
+    b_row = 8 if dtype == torch.float32 else 16  # (f32, u32) / (f64, u64) rows
     peak, peak_kind = measured_peaks()
 
     # synthetic input, resident in HBM (identical replica on every rank)
@@ -269,8 +269,8 @@ def run_ours(a):
         # host part of sectioned_sample (bit-exact binomial assignment) is
         # inside the sampling interval, as in the reference
         ak.assign_sections(N, S, M, r0.seed, r0.stream)
-        for (f, c, o, _) in passes:
-            sectioned_sample_into(table, S_eff, counts_d, offs_d, f, c, r0, out, o, rng_mode)
+        for (f, c, o, tot) in passes:
+            sectioned_sample_into(table, S_eff, counts_d, offs_d, f, c, r0, out, o, rng_mode, n_out=tot)
         e2.record()
         if record is not None:
             record.append((e0, e1, e2))
@@ -314,12 +314,12 @@ def run_ours(a):
         return statistics.median(ts)
 
     f0, c0, o0, d0 = passes[0]
-    t_pass = time_launch(lambda: sectioned_sample_into(table, S_eff, counts_d, offs_d, f0, c0, r0, out, o0, rng_mode))
+    t_pass = time_launch(lambda: sectioned_sample_into(table, S_eff, counts_d, offs_d, f0, c0, r0, out, o0, rng_mode, n_out=d0))
     pass_bytes = d0 * 8 + c0 * S_eff * b_row
     t_build1 = time_launch(lambda: ak.pack.build_table(ws, table))
     build_bytes = N * (2 * b_w + b_row)
     # reference-RNG (bit-exact mode) throughput of the same pass, for context
-    t_pass_ref = time_launch(lambda: sectioned_sample_into(table, S_eff, counts_d, offs_d, f0, c0, r0, out, o0, "reference"))
+    t_pass_ref = time_launch(lambda: sectioned_sample_into(table, S_eff, counts_d, offs_d, f0, c0, r0, out, o0, "reference", n_out=d0))
     # PSA+ (block prepack + residual PSA) on the same weights,
     # as a public-API call (it reads two counts back to the host), for context
     # (best of 5: the call waits on the host twice, so a descheduled host
@@ -383,7 +383,7 @@ def run_ours(a):
                 if od[i % 2] is None or od[i % 2].numel() < max(dr_e, 1):
                     od[i % 2] = torch.empty(max(dr_e, 1), dtype=torch.int64, device=dev)
                 sectioned_sample_into(te, asg_e.section_size, cd, odf, f_e, c_e, ak.RngStream(1, st_e),
-                                      od[i % 2], oo_e, rng_mode)
+                                      od[i % 2], oo_e, rng_mode, n_out=dr_e)
                 ev_cmp[i].record(s_cmp)
                 return dr_e
 

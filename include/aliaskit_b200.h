@@ -15,7 +15,11 @@
  *   - `stream` is a cudaStream_t (may be NULL = legacy default stream); calls
  *     are stream-ordered and asynchronous unless marked [sync];
  *   - scratch comes from a caller workspace sized by a *_workspace_bytes
- *     query; the library never frees caller memory and keeps no global state;
+ *     query; the library never frees caller memory.  Its only state is a
+ *     256-byte status buffer per (host thread, device, stream) for the
+ *     [sync] entry points that read back a flag or count (allocated on first
+ *     use, freed at thread exit); the device-attribute and kernel-attribute
+ *     set-up is done once per process;
  *   - every function returns an ak_status; Python wrappers map the codes 1:1
  *     onto the reference exceptions (model.py:32-46, split.py:28-33,
  *     pack.py:26-27, sample.py:40-41, stats.py:17-22).

@@ -117,17 +117,15 @@ def check(status: int, what: str = "", index: int | None = None, value=None):
     raise errors.from_status(status, msg, index=index, value=value)
 
 
-_ws_cache: dict = {}
-
-
 def workspace(nbytes: int, device: torch.device, tag: str = "default") -> torch.Tensor:
-    """A cached device scratch buffer of at least nbytes (per device/stream/tag)."""
-    key = (device.index, torch.cuda.current_stream(device).cuda_stream, tag)
-    buf = _ws_cache.get(key)
-    if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
-        _ws_cache[key] = buf
-    return buf
+    """Device scratch of at least nbytes for ONE call, from torch's caching
+    allocator.  The allocator is stream-ordered, so a buffer is only reused by
+    work queued after this call's kernels on the same stream; two host threads
+    (even on one shared stream) never receive the same live buffer, which a
+    process-wide cache keyed by stream could not guarantee.  ``tag`` is kept
+    for call-site readability."""
+    del tag
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
 
 
 def dtype_code(t: torch.dtype) -> int:

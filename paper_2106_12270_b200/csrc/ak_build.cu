@@ -1055,8 +1055,7 @@ int run_build(const void *wv, u64 n, double avg, void *rows, void *ws, cudaStrea
     }
     AK_CUDA_TRY(cudaMemsetAsync(W.counter, 0, 256, st));
     AK_CUDA_TRY(cudaMemsetAsync(W.status, 0, W.nst * 4, st));
-    AK_CUDA_TRY(cudaFuncSetAttribute(k_build_scan<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)ScanBuf<T>::BYTES));
+    AK_SMEM_ATTR(k_build_scan<T>, (int)ScanBuf<T>::BYTES);
     k_build_scan<T><<<(unsigned)W.nst, SC_WARPS * 32, ScanBuf<T>::BYTES, st>>>(w, n, avg, W);
     AK_LAUNCH_CHECK("k_build_scan");
     k_build_coarse<<<(unsigned)((W.nt + 1 + 255) / 256), 256, 0, st>>>(W, n);
@@ -1064,8 +1063,7 @@ int run_build(const void *wv, u64 n, double avg, void *rows, void *ws, cudaStrea
     k_build_split<T><<<(unsigned)((W.nt + 1 + NW - 1) / NW), TB, 0, st>>>(w, n, avg, W, O);
     AK_LAUNCH_CHECK("k_build_split");
     const size_t smem = sizeof(SecSmem);
-    AK_CUDA_TRY(cudaFuncSetAttribute(k_build_pack<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
+    AK_SMEM_ATTR(k_build_pack<T>, (int)smem);
     k_build_pack<T><<<(unsigned)(W.nt + 1), TB, smem, st>>>(w, n, avg, W, O,
                                                            (typename RowOf<T>::type *)rows);
     AK_LAUNCH_CHECK("k_build_pack");

@@ -40,7 +40,11 @@ int ak_check_launch(const char *where);
 static inline cudaStream_t ak_stream(void *s) { return (cudaStream_t)s; }
 
 int ak_num_sms();
-void *ak_stream_scratch(cudaStream_t st);  // 256 B per (device, stream), never freed
+void *ak_stream_scratch(cudaStream_t st);  // 256 B per (host thread, device, stream)
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the launch paths call this instead of the driver on every call
+cudaError_t ak_smem_attr_once(const void *kernel, int bytes);
+#define AK_SMEM_ATTR(kern, bytes) AK_CUDA_TRY(ak_smem_attr_once((const void *)(kern), (int)(bytes)))
 
 // ---------------------------------------------------------------------------
 // table rows

@@ -42,24 +42,50 @@ int ak_check_launch(const char *where)
     return AK_OK;
 }
 
-// 256 bytes of device scratch per (device, stream) for the small status
-// words the entry points read back (flags, counts): allocated once, so no
-// allocation sits on a call path; per stream, so concurrent calls on
-// different streams never share it.
+// 256 bytes of device scratch for the small status words an entry point
+// writes and reads back within ONE call (flags, counts).  Keyed by (host
+// thread, device, stream): two host threads that share a stream (e.g. both
+// on the legacy default stream) never share a buffer, and every call that
+// uses it ends with a stream synchronisation, so calls of one thread cannot
+// overlap.  Allocated once per key (no allocation on the call path) and
+// released when the thread exits.
+namespace {
+struct ThreadScratch {
+    std::map<std::pair<int, cudaStream_t>, void *> bufs;
+    ~ThreadScratch()
+    {
+        for (auto &kv : bufs) cudaFree(kv.second);
+    }
+};
+}  // namespace
+
 void *ak_stream_scratch(cudaStream_t st)
 {
-    static std::mutex mu;
-    static std::map<std::pair<int, cudaStream_t>, void *> bufs;
+    static thread_local ThreadScratch ts;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-    std::lock_guard<std::mutex> g(mu);
     auto key = std::make_pair(dev, st);
-    auto it = bufs.find(key);
-    if (it != bufs.end()) return it->second;
+    auto it = ts.bufs.find(key);
+    if (it != ts.bufs.end()) return it->second;
     void *p = nullptr;
     if (cudaMalloc(&p, 256) != cudaSuccess) return nullptr;
-    bufs[key] = p;
+    ts.bufs[key] = p;
     return p;
+}
+
+cudaError_t ak_smem_attr_once(const void *kernel, int bytes)
+{
+    static std::mutex mu;
+    static std::map<std::pair<const void *, int>, int> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(mu);
+    int &have = done[std::make_pair(kernel, dev)];
+    if (have >= bytes) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) have = bytes;
+    return e;
 }
 
 int ak_num_sms()

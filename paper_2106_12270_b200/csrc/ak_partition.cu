@@ -631,8 +631,7 @@ int run_plan(const double *lpre, u64 nl, const double *hpre, u64 nh, const void 
     } else {
         u64 runs = (s - 1 + PLAN_RUN - 1) / PLAN_RUN;
         size_t smem = PLAN_SMEM_DOUBLES * sizeof(double);
-        AK_CUDA_TRY(cudaFuncSetAttribute(k_plan_batched<T>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        AK_SMEM_ATTR(k_plan_batched<T>, (int)smem);
         k_plan_batched<T><<<(unsigned)runs, PLAN_RUN, smem, st>>>(A, (const T *)h_w);
         AK_LAUNCH_CHECK("k_plan_batched");
     }
@@ -655,8 +654,7 @@ int run_pack(const i64 *l_idx, const void *l_w, u64 nl, const i64 *h_idx, const 
         // shared memory; the staging schedule never changes the arithmetic.
         int c = cap > 512 ? 512 : (int)cap;
         size_t smem = (size_t)CH_WARPS * c * 32;
-        AK_CUDA_TRY(cudaFuncSetAttribute(k_pack_chunked<T>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        AK_SMEM_ATTR(k_pack_chunked<T>, (int)smem);
         k_pack_chunked<T><<<(unsigned)((cnt + CH_WARPS - 1) / CH_WARPS), CH_WARPS * 32, smem, st>>>(
             A, c);
         AK_LAUNCH_CHECK("k_pack_chunked");

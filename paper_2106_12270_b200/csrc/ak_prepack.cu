@@ -580,11 +580,11 @@ int ak_greedy_prepack(const void *w, int dtype, uint64_t n, double avg, uint32_t
     AK_CUDA_TRY(cudaMemsetAsync(rows, 0, n * rb, st));
     AK_CUDA_TRY(cudaMemsetAsync(nw, 0, 8, st));
     if (dtype == AK_F32) {
-        AK_CUDA_TRY(cudaFuncSetAttribute(k_prepack_block<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        AK_SMEM_ATTR(k_prepack_block<float>, (int)smem);
         k_prepack_block<float><<<(unsigned)nb, PP_TB, smem, st>>>((const float *)w, n, avg, block_size,
                                                                  threshold, (RowF32 *)rows, info);
     } else if (dtype == AK_F64) {
-        AK_CUDA_TRY(cudaFuncSetAttribute(k_prepack_block<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        AK_SMEM_ATTR(k_prepack_block<double>, (int)smem);
         k_prepack_block<double><<<(unsigned)nb, PP_TB, smem, st>>>((const double *)w, n, avg, block_size,
                                                                   threshold, (RowF64 *)rows, info);
     } else {

@@ -462,13 +462,18 @@ __global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
             if constexpr (SMODE == 2) generic_on(SoA64View{stw, sal}, ps, pe);
             else generic_on(tabp, ps, pe);
         };
-        if (MODE == AK_RNG_PHILOX4X32 && SMODE != 0 && pow2 && (sizeof(RowT) == 8 || n <= 0xFFFFFFFFull)) {
+        // the fast path counts calls linearly from cb: a section whose draw
+        // counters wrap past 2^64 (ctr0 + ib overflows) keeps the generic
+        // per-draw definition, call = (ctr0 + i) mod 2^64 >> 1
+        const bool ctr_wraps = (u64)ib > ~ctr0;
+        if (MODE == AK_RNG_PHILOX4X32 && SMODE != 0 && pow2 && !ctr_wraps &&
+            (sizeof(RowT) == 8 || n <= 0xFFFFFFFFull)) {
             // interior pairs q = p - p0 in [qa, qa + nfast): both draws in
             // range, the call counter's high word constant, whole CTA steps
             const i64 np = p1 - p0 + 1;
             const i64 qa = (2 * p0 - poff >= ia) ? 0 : 1;
             const i64 qb = np - ((2 * p1 - poff + 1 < ib) ? 0 : 1);
-            const u64 cb = (ctr0 >> 1) + (u64)p0;
+            const u64 cb = (ctr0 + (u64)(2 * p0 - poff)) >> 1;
             i64 nfast = qb > qa ? ((qb - qa) / (i64)blockDim.x) * (i64)blockDim.x : 0;
             if ((u64)(u32)cb + (u64)(qa + nfast) > 0xFFFFFFFFull) nfast = 0;
             if (nfast > 0) {
@@ -526,7 +531,7 @@ int launch_sectioned_t(const void *rows, u64 n, double avg, u64 S, const i64 *co
 {
     size_t smem = SMODE == 1 ? S * sizeof(RowT) : (SMODE == 2 ? S * 12 : 0);
     auto kern = k_sample_sectioned<RowT, MODE, SMODE>;
-    if (SMODE) AK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (SMODE) AK_SMEM_ATTR(kern, (int)smem);
     int per_sm = SMODE ? (smem > 110 * 1024 ? 1 : 2) : 2;
     u64 g = (u64)ak_num_sms() * per_sm;
     kern<<<(unsigned)g, 1024, smem, st>>>((const RowT *)rows, n, avg, S, counts, offsets, first,

@@ -223,6 +223,7 @@ int ak_soa_to_rows(const double *tw, const int64_t *alias, uint64_t n, int dtype
 int ak_count_unwritten(const void *rows, int dtype, uint64_t n, uint64_t *unwritten, void *stream)
 {
     cudaStream_t st = ak_stream(stream);
+    if (dtype != AK_F32 && dtype != AK_F64) return AK_ERR_VALUE;
     unsigned long long *c = (unsigned long long *)ak_stream_scratch(st);
     if (!c) return AK_ERR_CUDA;
     AK_CUDA_TRY(cudaMemsetAsync(c, 0, 16, st));

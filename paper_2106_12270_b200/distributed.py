@@ -93,4 +93,4 @@ class ShardedSectioned:
 
     def run(self, t: AliasTable, r: RngStream, out: torch.Tensor, rng: str = "reference") -> None:
         sectioned_sample_into(t, self.S, self.counts_d, self.offsets_d, self.first, self.count, r,
-                              out, self.out_off, rng)
+                              out, self.out_off, rng, n_out=self.draws)

@@ -58,6 +58,22 @@ def _rng_code(rng: str) -> int:
         raise ValueError(f"unknown rng mode {rng!r}: expected one of {sorted(_lib.RNG_MODES)}")
 
 
+def _check_out(out: torch.Tensor, need: int, dev: torch.device, what: str) -> None:
+    """A caller-supplied output buffer must be a contiguous int64 tensor on the
+    table's device with room for every draw the kernel writes through its raw
+    pointer; anything else raises instead of writing out of bounds."""
+    if not isinstance(out, torch.Tensor):
+        raise TypeError(f"{what}: out must be a torch.Tensor")
+    if out.dtype != torch.int64:
+        raise ValueError(f"{what}: out must be int64, got {out.dtype}")
+    if out.device != dev:
+        raise ValueError(f"{what}: out is on {out.device}, the table on {dev}")
+    if not out.is_contiguous():
+        raise ValueError(f"{what}: out must be contiguous")
+    if out.numel() < need:
+        raise ValueError(f"{what}: out holds {out.numel()} draws, {need} are written")
+
+
 def sample_one(t: AliasTable, r: RngStream) -> int:
     """One weighted draw (host uniform, one row read); advances r by one."""
     u = rng_uniform(r)
@@ -83,6 +99,8 @@ def sample_batch(t: AliasTable, m: int, r: RngStream, workers: int = 1, rng: str
     dev = t.rows.device
     if out is None:
         out = torch.empty(m, dtype=torch.int64, device=dev)
+    else:
+        _check_out(out, m, dev, "sample_batch")
     with torch.cuda.device(dev):
         _lib.check(_lib.lib().ak_sample_naive(
             _lib.ptr(t.rows), t.dtype_code, t.n, t.average, 0, t.n, r.seed, r.stream,
@@ -141,11 +159,28 @@ def assign_sections(n_rows: int, S: int, M: int, seed: int, stream: int = 0) -> 
 
 def sectioned_sample_into(t: AliasTable, S_eff: int, counts_d: torch.Tensor,
                           offsets_d: torch.Tensor, first: int, count: int, r: RngStream,
-                          out: torch.Tensor, out_base: int, rng: str = "reference") -> None:
+                          out: torch.Tensor, out_base: int, rng: str = "reference",
+                          n_out: int | None = None) -> None:
     """Draw sections [first, first+count) into out[offsets - out_base ...]
     without touching r (the building block of sectioned_sample and of the
-    multi-GPU / multi-pass drivers)."""
+    multi-GPU / multi-pass drivers).
+
+    ``out`` must hold offsets[last] + counts[last] - out_base draws; pass that
+    number as ``n_out`` when the host already knows it (the multi-pass drivers
+    do), otherwise it is read back from the device (one synchronisation)."""
     dev = t.rows.device
+    if count <= 0:
+        return
+    for name, x in (("counts", counts_d), ("offsets", offsets_d)):
+        if x.dtype != torch.int64 or x.device != dev or not x.is_contiguous():
+            raise ValueError(f"sectioned_sample: {name} must be contiguous int64 on {dev}")
+        if x.numel() < first + count:
+            raise ValueError(f"sectioned_sample: {name} has {x.numel()} entries, "
+                             f"sections [{first}, {first + count}) are drawn")
+    if n_out is None:
+        last = first + count - 1
+        n_out = int((offsets_d[last] + counts_d[last]).item()) - out_base
+    _check_out(out, n_out, dev, "sectioned_sample")
     with torch.cuda.device(dev):
         _lib.check(_lib.lib().ak_sample_sectioned(
             _lib.ptr(t.rows), t.dtype_code, t.n, t.average, S_eff, _lib.ptr(counts_d),
@@ -163,10 +198,12 @@ def sectioned_sample(t: AliasTable, S: int, M: int, r: RngStream, rng: str = "re
     dev = t.rows.device
     if out is None:
         out = torch.empty(M, dtype=torch.int64, device=dev)
+    else:
+        _check_out(out, M, dev, "sectioned_sample")
     if M:
         counts = torch.from_numpy(asg.counts).to(dev)
         offsets = torch.from_numpy(np.concatenate([[0], np.cumsum(asg.counts)[:-1]])).to(dev)
         sectioned_sample_into(t, asg.section_size, counts, offsets, 0, asg.n_sections, r, out, 0,
-                              rng)
+                              rng, n_out=M)
     r.counter += M
     return out

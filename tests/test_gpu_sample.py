@@ -197,6 +197,59 @@ def test_status_words_per_stream_threads():
     assert not errs, errs
 
 
+def test_threads_share_default_stream():
+    """host threads that all use the default stream must not share
+    scratch.  Four threads build different tables and read status words back
+    concurrently on the default stream; every result must equal the
+    single-threaded one."""
+    import threading
+
+    sets = [ak.make_weight_set(random_weights(np.random.default_rng(50 + k), 200_000 + 977 * k))
+            for k in range(4)]
+    want = [ak.psa_construct(ws).to_numpy() for ws in sets]
+    bad = torch.tensor([0, 1], device=DEV)
+    good = torch.tensor([1, 2, 2], device=DEV)
+    errs = []
+
+    def worker(k):
+        try:
+            for it in range(6):
+                tw, al = ak.psa_construct(sets[k]).to_numpy()
+                assert np.array_equal(al, want[k][1]) and np.array_equal(tw, want[k][0])
+                if (k + it) % 2:
+                    with pytest.raises(ak.IndexOutOfRange):
+                        ak.frequency_counts(bad, 3)
+                else:
+                    assert ak.frequency_counts(good, 3).tolist() == [1, 2, 0]
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+
+
+def test_out_buffer_is_checked():
+    """a caller-supplied out tensor is validated before the kernel
+    writes through its pointer."""
+    t = ak.psa_construct(ak.make_weight_set(np.arange(1.0, 101.0)))
+    r = ak.RngStream(1)
+    for bad in (torch.empty(9, dtype=torch.int64, device=DEV),             # too short
+                torch.empty(10, dtype=torch.int32, device=DEV),            # wrong dtype
+                torch.empty(20, dtype=torch.int64, device=DEV)[::2],       # strided
+                torch.empty(10, dtype=torch.int64)):                       # host
+        with pytest.raises(ValueError):
+            ak.sample_batch(t, 10, r, out=bad)
+        with pytest.raises(ValueError):
+            ak.sectioned_sample(t, 16, 10, r, out=bad)
+    assert r.counter == 0  # nothing drawn
+    ok = torch.empty(10, dtype=torch.int64, device=DEV)
+    assert ak.sample_batch(t, 10, r, out=ok) is ok
+
+
 def philox4x32_words(call: np.ndarray, strm: int, seed: int):
     """numpy Philox4x32-10 (Random123 constants) of counters (call lo, call
     hi, strm lo, strm hi) under key (seed lo, seed hi): the two 64-bit words
