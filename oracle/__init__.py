@@ -64,6 +64,7 @@ def lib():
         L.ako_validate_table.argtypes = [vp, vp, vp, u64, dbl, vp, vp, vp]
         L.ako_vose.argtypes = [vp, u64, dbl, vp, vp]
         L.ako_vose_quad.argtypes = [vp, u64, dbl, vp, vp]
+        L.ako_vose_fixed.argtypes = [vp, u64, dbl, vp, vp]
         L.ako_exclusive_prefix.argtypes = [vp, u64, vp]
         L.ako_partition.restype = u64
         L.ako_partition.argtypes = [vp, u64, dbl, vp, vp, vp, vp, vp, vp, vp]
@@ -195,6 +196,17 @@ def vose_construct_quad(w, total: float) -> Table:
     tw = np.zeros(n)
     alias = np.zeros(n, dtype=np.int64)
     lib().ako_vose_quad(_p(w), n, total / n, _p(tw), _p(alias))
+    return Table(tw, alias, n, total)
+
+
+def vose_construct_fixed(w, total: float) -> Table:
+    """Vose in the device builder's exact fixed-point arithmetic (diagnostic:
+    the table psa_construct must reproduce bit for bit; see ako_vose_fixed)."""
+    w = _f64(w)
+    n = w.size
+    tw = np.zeros(n)
+    alias = np.zeros(n, dtype=np.int64)
+    lib().ako_vose_fixed(_p(w), n, total / n, _p(tw), _p(alias))
     return Table(tw, alias, n, total)
 
 

@@ -128,6 +128,14 @@ def workspace(nbytes: int, device: torch.device, tag: str = "default") -> torch.
     return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
 
 
+def aligned32(t: torch.Tensor) -> torch.Tensor:
+    """t itself when its data is 32-byte aligned (the builder's 256-bit loads
+    and stores need it), else a contiguous aligned copy."""
+    if t.data_ptr() % 32 == 0 and t.is_contiguous():
+        return t
+    return t.contiguous().clone()
+
+
 def dtype_code(t: torch.dtype) -> int:
     if t == torch.float32:
         return F32

@@ -99,8 +99,9 @@ def build_table(w: WeightSet, out: AliasTable | None = None) -> AliasTable:
         out = AliasTable.empty(w.n, w.total, dt, dev)
     L = _lib.lib()
     ws = _lib.workspace(L.ak_build_workspace_bytes(w.n, _lib.dtype_code(dt)), dev, "build")
+    wt = _lib.aligned32(w.weights)  # held until the call is queued
     with torch.cuda.device(dev):
-        _lib.check(L.ak_build_psa(_lib.ptr(w.weights), _lib.dtype_code(dt), w.n, w.total,
+        _lib.check(L.ak_build_psa(_lib.ptr(wt), _lib.dtype_code(dt), w.n, w.total,
                                   _lib.ptr(out.rows), _lib.ptr(ws), ws.numel(),
                                   _lib.stream_ptr(dev)), "build_psa")
     return out
@@ -111,7 +112,7 @@ def psa_construct(w: WeightSet, s: int = 64, workers: int = 1, chunked: bool = F
     """Split construction (pack.py:255-277) as the fused device pipeline.
 
     ``s``, ``workers``, ``chunked`` and ``chunk_capacity`` are validated as in
-    the reference; the device pipeline sections the work by 2048-item tiles
+    the reference; the device pipeline sections the work by 512-item chunks
     itself, and (like the reference, whose output is section- and
     worker-invariant up to rounding) its table does not depend on them.
     """

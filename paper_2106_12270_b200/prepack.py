@@ -82,6 +82,7 @@ def psa_plus_construct(w: WeightSet, s: int = 64, block_size: int = 4096,
     if k:
         rt = torch.empty(2 * k, dtype=torch.int64, device=dev)  # f64 rows over residual positions
         ws = _lib.workspace(L.ak_build_workspace_bytes(k, _lib.F64), dev, "build")
+        res_w = _lib.aligned32(res_w)
         with torch.cuda.device(dev):
             _lib.check(L.ak_build_psa_avg(_lib.ptr(res_w), _lib.F64, k, w.average, _lib.ptr(rt),
                                           _lib.ptr(ws), ws.numel(), _lib.stream_ptr(dev)),
