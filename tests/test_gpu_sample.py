@@ -204,7 +204,7 @@ def test_threads_share_default_stream():
     single-threaded one."""
     import threading
 
-    sets = [ak.make_weight_set(random_weights(np.random.default_rng(50 + k), 200_000 + 977 * k))
+    sets = [ak.make_weight_set(random_weights(np.random.default_rng(50 + k), 200_000 + 977 * k, k % 3))
             for k in range(4)]
     want = [ak.psa_construct(ws).to_numpy() for ws in sets]
     bad = torch.tensor([0, 1], device=DEV)
