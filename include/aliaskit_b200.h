@@ -74,6 +74,13 @@ int ak_fill_uniform(uint64_t seed, uint64_t stream_id, uint64_t ctr0, uint64_t m
 /* Raw Philox2x64-10 words (both lanes) for known-answer tests. */
 int ak_philox2x64(const uint64_t *ctr, const uint64_t *strm, const uint64_t *key, uint64_t m,
                   uint64_t *out_w0, uint64_t *out_w1, void *stream);
+/* Raw Philox4x32-10 (Random123 constants; the GPU-native RNG mode) for
+ * known-answer tests: ctr 4 words and key 2 words per input; out 12 words
+ * per input = the generic, inline-key and round-key-table formulations the
+ * samplers use (all three must agree).  Not a reference call site: the
+ * reference has only Philox2x64-10 (rng.py). */
+int ak_philox4x32(const uint32_t *ctr, const uint32_t *key, uint64_t m, uint32_t *out,
+                  void *stream);
 /* derive_stream (rng.py:167-169) [host]. */
 uint64_t ak_derive_stream(uint64_t seed, uint64_t stream_id, uint64_t tag0, uint64_t tag1);
 

@@ -65,6 +65,7 @@ def lib():
         L.ako_vose.argtypes = [vp, u64, dbl, vp, vp]
         L.ako_vose_quad.argtypes = [vp, u64, dbl, vp, vp]
         L.ako_vose_fixed.argtypes = [vp, u64, dbl, vp, vp]
+        L.ako_vose_fixed_margins.argtypes = [vp, u64, dbl, vp, u64, vp]
         L.ako_exclusive_prefix.argtypes = [vp, u64, vp]
         L.ako_partition.restype = u64
         L.ako_partition.argtypes = [vp, u64, dbl, vp, vp, vp, vp, vp, vp, vp]
@@ -208,6 +209,17 @@ def vose_construct_fixed(w, total: float) -> Table:
     alias = np.zeros(n, dtype=np.int64)
     lib().ako_vose_fixed(_p(w), n, total / n, _p(tw), _p(alias))
     return Table(tw, alias, n, total)
+
+
+def decision_margins(w, total: float, rows) -> np.ndarray:
+    """Exact decision margins (units of avg) of 1-based ``rows`` in Vose's
+    order (ako_vose_fixed_margins): how far each row's alias/threshold
+    decision is from flipping.  Certifies near-ties at any N in O(N)."""
+    w = _f64(w)
+    rows = np.ascontiguousarray(np.sort(np.asarray(rows, dtype=np.int64)))
+    out = np.empty(rows.size)
+    lib().ako_vose_fixed_margins(_p(w), w.size, total / w.size, _p(rows), rows.size, _p(out))
+    return out
 
 
 def partition_items(w, total: float):

@@ -33,6 +33,7 @@ _SIGS = {
     "ak_row_bytes": (sz, [ci]),
     "ak_fill_uniform": (ci, [u64, u64, u64, u64, vp, vp]),
     "ak_philox2x64": (ci, [vp, vp, vp, u64, vp, vp, vp]),
+    "ak_philox4x32": (ci, [vp, vp, u64, vp, vp]),
     "ak_derive_stream": (u64, [u64, u64, u64, u64]),
     "ak_weights_workspace_bytes": (sz, [u64]),
     "ak_weights_validate_total": (ci, [vp, ci, u64, vp, vp, vp, sz, vp]),

@@ -40,6 +40,12 @@ __global__ void k_philox_raw(const u64 *ctr, const u64 *strm, const u64 *key, u6
     w1[i] = b;
 }
 
+// Philox4x32-10 for known-answer tests, through each formulation the
+// samplers use: the generic round loop (ak_philox4x32_10), round keys formed
+// inline (philox4x32_key) and round keys as a precomputed table
+// (philox4x32_rk).  out holds 12 words per input: generic, inline, table.
+__global__ void k_philox4x32_raw(const u32 *ctr, const u32 *key, u64 m, u32 *out);
+
 // Fast mode: the uniform of counter v (64-bit) is word (v & 1) of
 // Philox4x32-10(counter = (v >> 1, stream), key = seed).
 __device__ __forceinline__ void ph4_pair(u64 call, u64 strm, u64 seed, double &u0, double &u1)
@@ -222,6 +228,31 @@ __device__ __forceinline__ uint4 philox4x32_rk(uint4 c, const Ph4Keys &rk)
         c = make_uint4(hi1 ^ c.y ^ rk.k[2 * r], lo1, hi0 ^ c.w ^ rk.k[2 * r + 1], lo0);
     }
     return c;
+}
+
+__global__ void k_philox4x32_raw(const u32 *ctr, const u32 *key, u64 m, u32 *out)
+{
+    const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const uint4 c = make_uint4(ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3]);
+    const u32 k0 = key[2 * i], k1 = key[2 * i + 1];
+    Ph4Keys rk;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        rk.k[2 * r] = k0 + (u32)r * AK_PH4_W0;
+        rk.k[2 * r + 1] = k1 + (u32)r * AK_PH4_W1;
+    }
+    const uint4 a = ak_philox4x32_10(c, make_uint2(k0, k1));
+    const uint4 b = philox4x32_key(c, k0, k1);
+    const uint4 d = philox4x32_rk(c, rk);
+    const uint4 r3[3] = {a, b, d};
+#pragma unroll
+    for (int v = 0; v < 3; ++v) {
+        out[12 * i + 4 * v] = r3[v].x;
+        out[12 * i + 4 * v + 1] = r3[v].y;
+        out[12 * i + 4 * v + 2] = r3[v].z;
+        out[12 * i + 4 * v + 3] = r3[v].w;
+    }
 }
 
 // the bucket rule for one 64-bit word on a staged f32 section of span 2^b
@@ -577,6 +608,15 @@ int ak_fill_uniform(uint64_t seed, uint64_t stream_id, uint64_t ctr0, uint64_t m
     if (m == 0) return AK_OK;
     k_fill_uniform<<<grid_for(m, 256), 256, 0, ak_stream(stream)>>>(seed, stream_id, ctr0, m, out);
     AK_LAUNCH_CHECK("k_fill_uniform");
+    return AK_OK;
+}
+
+int ak_philox4x32(const uint32_t *ctr, const uint32_t *key, uint64_t m, uint32_t *out,
+                  void *stream)
+{
+    if (m == 0) return AK_OK;
+    k_philox4x32_raw<<<(unsigned)((m + 255) / 256), 256, 0, ak_stream(stream)>>>(ctr, key, m, out);
+    AK_LAUNCH_CHECK("k_philox4x32_raw");
     return AK_OK;
 }
 

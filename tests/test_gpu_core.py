@@ -35,6 +35,48 @@ def test_philox_kats_on_device(hand):
     assert got1 == [int(x, 16) for x in hand["philox2x64_10_kat_w1_random123"]]
 
 
+def philox4x32_np(c, k):
+    """Philox4x32-10 (Random123 constants), the restatement the KATs pin."""
+    M0, M1, W0, W1 = 0xD2511F53, 0xCD9E8D57, 0x9E3779B9, 0xBB67AE85
+    c, k = list(c), list(k)
+    for _ in range(10):
+        p0, p1 = M0 * c[0], M1 * c[2]
+        c = [(p1 >> 32) ^ c[1] ^ k[0], p1 & 0xFFFFFFFF, (p0 >> 32) ^ c[3] ^ k[1], p0 & 0xFFFFFFFF]
+        k = [(k[0] + W0) & 0xFFFFFFFF, (k[1] + W1) & 0xFFFFFFFF]
+    return c
+
+
+# Random123 known-answer vectors for philox4x32_10 (kat_vectors)
+PHILOX4X32_KATS = [
+    ((0, 0, 0, 0), (0, 0), (0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8)),
+    ((0xFFFFFFFF,) * 4, (0xFFFFFFFF, 0xFFFFFFFF), (0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD)),
+    ((0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344), (0xA4093822, 0x299F31D0),
+     (0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1)),
+]
+
+
+def test_philox4x32_kats_on_device(rng):
+    """The GPU-native RNG (rng="philox4x32") against Random123's published
+    answers, through all three formulations the samplers compile (generic
+    loop, inline round keys, round-key table), plus random inputs against
+    the restatement."""
+    ins = [(c, k) for c, k, _ in PHILOX4X32_KATS]
+    for _ in range(200):
+        ins.append((tuple(int(x) for x in rng.integers(0, 2**32, 4)), tuple(int(x) for x in rng.integers(0, 2**32, 2))))
+    m = len(ins)
+    as_i32 = lambda xs: torch.tensor([x - (1 << 32) if x >= (1 << 31) else x for x in xs], dtype=torch.int32, device=DEV)
+    ctr = as_i32([x for c, _ in ins for x in c])
+    key = as_i32([x for _, k in ins for x in k])
+    out = torch.empty(12 * m, dtype=torch.int32, device=DEV)
+    _lib.check(_lib.lib().ak_philox4x32(ctr.data_ptr(), key.data_ptr(), m, out.data_ptr(), _lib.stream_ptr()))
+    got = [x & 0xFFFFFFFF for x in out.cpu().tolist()]
+    for i, (c, k) in enumerate(ins):
+        want = list(PHILOX4X32_KATS[i][2]) if i < 3 else philox4x32_np(c, k)
+        assert philox4x32_np(c, k) == want  # the restatement reproduces the KATs
+        for v in range(3):
+            assert got[12 * i + 4 * v:12 * i + 4 * v + 4] == want, (i, v)
+
+
 def test_uniform_block_golden_and_wrap(golden):
     r = ak.RngStream(20260815)
     assert np.array_equal(ak.uniform_block(r, 1000).cpu().numpy(), golden["ub_a"])
@@ -204,6 +246,50 @@ def test_plan_hand_and_validation(hand):
     with pytest.raises(ak.InvalidSectionCount):
         ak.compute_split_plan(p, 5)
     assert ak.binary_search_boundary(p, 0, 0.0) == (0, 0, 0.0)
+
+
+def _boundary_ref(lpre, hpre, hw, n_i, cap):
+    """split.py:107-137 restated over numpy arrays (the reference loop)."""
+    nl, nh = lpre.size - 1, hpre.size - 1
+    lo, hi = max(0, n_i - nl), min(n_i, nh)
+    best, a, b = lo, lo, hi
+    while a <= b:
+        mid = (a + b) >> 1
+        if lpre[n_i - mid] + hpre[mid] <= cap:
+            best, a = mid, mid + 1
+        else:
+            b = mid - 1
+    h, l = best, n_i - best
+    taken = cap - (float(lpre[l]) + float(hpre[h]))
+    spill = max(float(hw[h]) - taken, 0.0) if h < nh and taken > 0.0 else 0.0
+    return l, h, spill
+
+
+def test_binary_search_boundary_real_boundaries(rng):
+    """a5: the scalar boundary search equals the plan kernel at every real
+    boundary (n_i = floor(i N / s), cap = n_i * avg), as the reference's own
+    cross-check does (tests/test_split.py:76-88), and equals the reference
+    loop restated at arbitrary (n_i, cap) pairs on the same prefix arrays."""
+    for trial in range(12):
+        n = int(rng.integers(50, 20_000))
+        w = random_weights(rng, n, trial % 5)
+        p = ak.partition_items(ak.make_weight_set(w))
+        s = int(rng.integers(2, min(n, 300)))
+        plan = ak.compute_split_plan(p, s)
+        lpre, hpre = p.lprefix.cpu().numpy(), p.hprefix.cpu().numpy()
+        hw = p.h_weight.cpu().numpy()
+        lc, hc, sp = O.compute_split_plan(lpre, hpre, hw, n, s, p.avg)
+        for i in range(1, s):
+            n_i = i * n // s
+            got = ak.binary_search_boundary(p, n_i, n_i * p.avg)
+            assert got == (int(lc[i]), int(hc[i]), float(sp[i])), (trial, i)
+            assert got == plan.boundaries[i]
+        for _ in range(40):
+            n_i = int(rng.integers(0, n + 1))
+            cap = float(rng.uniform(0, 1.2)) * n_i * p.avg
+            assert ak.binary_search_boundary(p, n_i, cap) == _boundary_ref(lpre, hpre, hw, n_i, cap)
+    with pytest.raises(ValueError):
+        ak.binary_search_boundary(p, n + 1, 0.0)
 
 
 @pytest.mark.parametrize("cap", [0, 2, 3, 64, 10**6])

@@ -138,3 +138,17 @@ def test_live_reference_assignment(reference, rng):
         seed = int(rng.integers(2**63))
         assert np.array_equal(A.assign_sections(n, S, M, seed, stream=2).counts,
                               O.assign_sections(n, S, M, seed, 2))
+
+
+def test_decision_margins_pinned(rng):
+    """The O(N) exact margins (oracle decision_margins, fixed-point keys)
+    equal the exact fsum-based nearest-key distances of conftest."""
+    from conftest import near_tie_margins
+
+    for n, kind in ((40, 3), (300, 0), (1500, 1), (900, 2)):
+        w = random_weights(rng, n, kind)
+        _, total = O.make_weight_set(w)
+        rows = np.arange(1, n + 1)
+        a = O.decision_margins(w, total, rows)
+        b = np.array(near_tie_margins(w, total, rows))
+        assert np.max(np.abs(a - b)) < 1e-10
