@@ -225,6 +225,22 @@ size_t ak_validate_workspace_bytes(uint64_t n);
 int ak_validate_table(const void *rows, int dtype, uint64_t n, const void *w, int w_dtype,
                       double avg, double row_tol, int *rows_ok, double *worst_rel,
                       int64_t *worst_item, void *ws, size_t ws_bytes, void *stream);
+/* [sync] validate_table for the items [item_lo, item_hi): every row is
+ * read (its donation may land in the range), the row invariants are checked
+ * for the rows of the range, the per-item mass for the items of the range.
+ * Ranks of a sharded validation take disjoint ranges and reduce the three
+ * results (min ok, max worst, min worst item among the maxima); the union
+ * equals ak_validate_table.  Workspace: ak_validate_workspace_bytes(range). */
+int ak_validate_table_range(const void *rows, int dtype, uint64_t n, uint64_t item_lo,
+                            uint64_t item_hi, const void *w, int w_dtype, double avg,
+                            double row_tol, int *rows_ok, double *worst_rel, int64_t *worst_item,
+                            void *ws, size_t ws_bytes, void *stream);
+/* chi_square_test's sums (stats.py:84-121) over bins [0, m) of a counts
+ * shard with their weights: out4 = {sum over kept bins of (c-e)^2/e, kept
+ * bins, pooled observed, pooled expected}, e_i = draws * w_i / total_w, a
+ * bin kept iff e_i >= 5 (device doubles; shards add up). */
+int ak_chi2_partial(const int64_t *counts, const void *w, int w_dtype, uint64_t m,
+                    double total_w, double draws, double *out4, void *stream);
 /* [sync] frequency_counts (stats.py:25-32): counts[i] = #samples == i+1. */
 int ak_frequency_counts(const int64_t *samples, uint64_t m, uint64_t n, int64_t *counts,
                         void *stream);

@@ -59,7 +59,9 @@ _SIGS = {
                                  ci, vp]),
     "ak_validate_workspace_bytes": (sz, [u64]),
     "ak_validate_table": (ci, [vp, ci, u64, vp, ci, dbl, dbl, vp, vp, vp, vp, sz, vp]),
+    "ak_validate_table_range": (ci, [vp, ci, u64, u64, u64, vp, ci, dbl, dbl, vp, vp, vp, vp, sz, vp]),
     "ak_frequency_counts": (ci, [vp, u64, u64, vp, vp]),
+    "ak_chi2_partial": (ci, [vp, vp, ci, u64, dbl, dbl, vp, vp]),
     "ak_rows_to_soa": (ci, [vp, ci, u64, vp, vp, vp]),
     "ak_soa_to_rows": (ci, [vp, vp, u64, ci, vp, vp]),
     "ak_count_unwritten": (ci, [vp, ci, u64, vp, vp]),

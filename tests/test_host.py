@@ -50,6 +50,13 @@ def _free_port():
 
 
 def _worker(rank, world, port, q):
+    """One rank: the PRODUCT's host-side sharding (naive_shard, the host C++
+    binomial assignment behind assign_sections, section_shard) plans its
+    share; its draws come from the oracle sampler here, as the product's
+    samplers need a GPU (tests/test_gpu_multi.py runs the same plan on the
+    device through the product end to end)."""
+    import paper_2106_12270_b200 as ak
+
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -61,12 +68,22 @@ def _worker(rank, world, port, q):
     m = 10_001
     off, cnt = D.naive_shard(m, rank, world)
     part = O.sample_batch(t, cnt, seed=42, stream=3, counter=100 + off)
-    # sectioned: each rank recomputes the counts and draws its section run
+    # sectioned: each rank recomputes the counts (product host C++) and draws
+    # its section run, section by section with the reference's per-section
+    # streams
     S, M = 16, 20_000
-    counts = O.assign_sections(t.n, S, M, 42, 5)
-    first, count, out_off, draws = D.section_shard(counts, rank, world)
-    full = O.sectioned_sample(t, S, M, 42, 5, 9)  # reference slice to compare
-    mine = full[out_off:out_off + draws]
+    asg = ak.assign_sections(t.n, S, M, 42, 5)
+    first, count, out_off, draws = D.section_shard(asg.counts, rank, world)
+    pieces = []
+    for j in range(first, first + count):
+        lo, hi = j * S, min((j + 1) * S, t.n)
+        strm = O.derive_stream(42, 5, j, O.SALT_SECTION)
+        pieces.append(O.rule(t.tw, t.alias, t.total / t.n,
+                             O.uniform_block(42, strm, 9, int(asg.counts[j])), lo, hi - lo))
+    mine = np.concatenate(pieces) if pieces else np.empty(0, dtype=np.int64)
+    assert mine.size == draws
+    # the product's host counts equal the oracle's on every rank
+    assert np.array_equal(asg.counts, O.assign_sections(t.n, S, M, 42, 5))
     parts = [None] * world
     dist.all_gather_object(parts, (part.tolist(), out_off, mine.tolist()))
     if rank == 0:
