@@ -249,6 +249,11 @@ int ak_rows_to_soa(const void *rows, int dtype, uint64_t n, double *tw, int64_t 
                    void *stream);
 int ak_soa_to_rows(const double *tw, const int64_t *alias, uint64_t n, int dtype, void *rows,
                    void *stream);
+/* Rows [first, first+count) as ALT1 file rows (io.py:21): 16 bytes each, f64
+ * threshold then u64 alias, into out (device) — the streamed save_table's
+ * widening of f32 tables, chunk by chunk. */
+int ak_rows_to_alt1(const void *rows, int dtype, uint64_t n, uint64_t first, uint64_t count,
+                    void *out, void *stream);
 /* [sync] count of rows with alias == 0 (pack.py:275-276 check) */
 int ak_count_unwritten(const void *rows, int dtype, uint64_t n, uint64_t *unwritten,
                        void *stream);

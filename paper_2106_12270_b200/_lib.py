@@ -65,6 +65,7 @@ _SIGS = {
     "ak_rows_to_soa": (ci, [vp, ci, u64, vp, vp, vp]),
     "ak_soa_to_rows": (ci, [vp, vp, u64, ci, vp, vp]),
     "ak_count_unwritten": (ci, [vp, ci, u64, vp, vp]),
+    "ak_rows_to_alt1": (ci, [vp, ci, u64, u64, u64, vp, vp]),
 }
 
 

@@ -11,7 +11,7 @@
 //   ak_validate_table_range  the same for an item range (sharded validation)
 //   ak_frequency_counts  frequency_counts (stats.py:25-32)
 //   ak_chi2_partial      chi_square_test's sums over a bin range (stats.py:84-121)
-//   ak_rows_to_soa / ak_soa_to_rows / ak_count_unwritten
+//   ak_rows_to_soa / ak_soa_to_rows / ak_rows_to_alt1 / ak_count_unwritten
 #include "ak_common.cuh"
 
 namespace {
@@ -142,6 +142,17 @@ __global__ void k_to_soa(const RowT *__restrict__ rows, u64 n, double *tw, i64 *
         RowT r = rows[i];
         tw[i] = (double)r.tw;
         alias[i] = (i64)r.alias;
+    }
+}
+
+// rows [first, first+count) as ALT1 file rows (f64 threshold, u64 alias)
+template <typename RowT>
+__global__ void k_to_alt1(const RowT *__restrict__ rows, u64 first, u64 count, double2 *out)
+{
+    u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+        const RowT r = rows[first + i];
+        out[i] = make_double2((double)r.tw, __longlong_as_double((long long)(u64)r.alias));
     }
 }
 
@@ -302,6 +313,19 @@ int ak_soa_to_rows(const double *tw, const int64_t *alias, uint64_t n, int dtype
     else if (dtype == AK_F64) k_from_soa<RowF64><<<grid_of(n), 256, 0, st>>>(tw, alias, n, (RowF64 *)rows);
     else return AK_ERR_VALUE;
     AK_LAUNCH_CHECK("k_from_soa");
+    return AK_OK;
+}
+
+int ak_rows_to_alt1(const void *rows, int dtype, uint64_t n, uint64_t first, uint64_t count,
+                    void *out, void *stream)
+{
+    if (first > n || count > n - first) return AK_ERR_VALUE;
+    if (count == 0) return AK_OK;
+    cudaStream_t st = ak_stream(stream);
+    if (dtype == AK_F32) k_to_alt1<RowF32><<<grid_of(count), 256, 0, st>>>((const RowF32 *)rows, first, count, (double2 *)out);
+    else if (dtype == AK_F64) k_to_alt1<RowF64><<<grid_of(count), 256, 0, st>>>((const RowF64 *)rows, first, count, (double2 *)out);
+    else return AK_ERR_VALUE;
+    AK_LAUNCH_CHECK("k_to_alt1");
     return AK_OK;
 }
 

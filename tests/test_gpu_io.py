@@ -76,3 +76,54 @@ def test_bench_rows_on_device():
     assert all(r["throughput_per_s"] > 0 and "backend=b200" in r["param"] for r in rows)
     assert [r["s"] for r in med] == [1, 64, 64, 0, 1024]
     assert rows_to_csv(rows).count("\n") == len(rows) + 1
+
+
+_STREAM_SCRIPT = r"""
+import os, sys, torch
+sys.path.insert(0, os.environ["AK_ROOT"])
+import paper_2106_12270_b200 as ak
+
+def hwm():
+    for line in open("/proc/self/status"):
+        if line.startswith("VmHWM"):
+            return int(line.split()[1]) * 1024
+dt = torch.float32 if sys.argv[1] == "f32" else torch.float64
+n, path = int(sys.argv[2]), sys.argv[3]
+ws = ak.gen_uniform(n, ak.RngStream(seed=5), dtype=dt)
+t = ak.psa_construct(ws)
+torch.cuda.synchronize()
+base = hwm()
+ak.save_table(t, path)
+ak.save_weights(ws, path + ".w")
+u = ak.load_table(path)
+v = ak.load_weights(path + ".w")
+peak = hwm() - base
+same_rows = torch.equal(u.rows.view(torch.float64)[0::2].to(t.rows.device),
+                        (t.rows.view(torch.float32)[0::2].double() if dt == torch.float32
+                         else t.rows.view(torch.float64)[0::2]))
+same_alias = torch.equal(u.rows[1::2], (t.rows.view(torch.int32)[1::2].long() if dt == torch.float32
+                                       else t.rows[1::2]))
+same_w = torch.equal(v.weights, ws.weights.double()) and v.total == ak.make_weight_set(ws.weights.double()).total
+print(peak, os.path.getsize(path), int(same_rows), int(same_alias), int(same_w))
+"""
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_streaming_round_trip_1e8_bounded_host_memory(tmp_path, dtype):
+    """N = 1e8: the table (1.6 GB ALT1) and weights round-trip bit-exactly
+    through the streamed writers/readers, and the process's host memory grows
+    by about the two pinned chunk buffers (2 x 64 MB), not by the file size."""
+    import os
+    import subprocess
+    import sys
+
+    n = 10**8
+    path = str(tmp_path / "t.alt")
+    env = dict(os.environ, AK_ROOT=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    out = subprocess.run([sys.executable, "-c", _STREAM_SCRIPT, dtype, str(n), path], env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    peak, size, same_rows, same_alias, same_w = (int(x) for x in out.stdout.split()[-5:])
+    assert size == 20 + 16 * n
+    assert same_rows and same_alias and same_w
+    assert peak < 512 * 2**20, f"host memory grew by {peak / 2**20:.0f} MiB"
