@@ -41,7 +41,7 @@ for _ in range(a.reps):
     ts.append(e0.elapsed_time(e1))
 ts.sort()
 b = 4 if dt == torch.float32 else 8
-byts = N * (2 * b + b + 4)
+byts = N * (2 * b + 2 * b)  # read w twice + write the row (8 B f32 / 16 B f64)
 med = ts[len(ts) // 2]
 print(f"{a.method} N={N:.0e} {a.dist} {a.dtype}: median {med:.3f} ms  min {ts[0]:.3f} ms  "
       f"{N / med / 1e6:.1f} G items/s  {byts / med / 1e6:.0f} GB/s algorithmic")
