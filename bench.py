@@ -54,8 +54,14 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--cpu-n", type=float, default=1e8)
     ap.add_argument("--cpu-samples", type=float, default=2e8)
+    ap.add_argument("--ref-samples", type=float, default=1e8,
+                    help="reference arm: draws per step (sectioned and naive each) from the N=1e9 table")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-f64", action="store_true", help="skip the C5 float64 build/sampling legs")
+    ap.add_argument("--broadcast", action="store_true",
+                    help="N>1: rank 0 builds the table and NCCL-broadcasts it every step "
+                         "(instead of every rank rebuilding it from the replicated weights)")
     return ap.parse_args()
 
 
@@ -149,33 +155,86 @@ def cpu_baseline(n_items: int, n_samples: int, section: int, threads: int):
     }
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_weights(n: int) -> np.ndarray:
+    """The GPU arm's weights, bit for bit: gen_uniform(n, RngStream(seed=1))
+    cast to float32 (weightgen.py:15-24: Philox uniforms, exact zeros redrawn
+    at fresh counters), upcast to float64 for the f64-only reference."""
+    import oracle as O
+
+    w = O.uniform_block(1, 0, 0, n)
+    ctr = n
+    z = np.flatnonzero(w == 0.0)
+    while z.size:
+        w[z] = O.uniform_block(1, 0, ctr, z.size)
+        ctr += z.size
+        z = z[w[z] == 0.0]
+    return w.astype(np.float32).astype(np.float64)
+
+
 def run_reference(a):
+    """The reference algorithm on the host cores (oracle/ C restatement of
+    aliaskit; the reference is Python + numba, so there is no oracle/_ref):
+    the GPU arm's workload — the same N=1e9 float32 uniform weights (bit-
+    identical), PSA construction (s = N/65536, all cores), then per step a
+    bounded sample of the same sampling workload: sectioned draws (S, stream
+    RngStream(1, 7), serial as in the reference) and naive draws (<= 16
+    workers, sample.py:132), each timed separately."""
+    import oracle as O
+
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    n_items, n_samples = int(a.cpu_n), int(a.cpu_samples)
-    vals = []
-    detail = None
+    N = int(a.n)
+    Mr = int(a.ref_samples)
+    w = reference_weights(N)
+    _, tot = O.make_weight_set(w)
+    t0 = time.perf_counter()
+    table = O.psa_construct(w, tot, s=max(64, N // 65536), workers=threads)
+    t_build = time.perf_counter() - t0
+    del w
+    sec, nai = [], []
     for i in range(a.warmup + a.steps):
-        d = cpu_baseline(n_items, n_samples, a.section, threads)
+        t0 = time.perf_counter()
+        O.sectioned_sample(table, a.section, Mr, 1, 7, i * Mr)
+        ts = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        O.sample_batch(table, Mr, 1, 8, i * Mr, workers=min(threads, 16))
+        tn = time.perf_counter() - t0
         if i >= a.warmup:
-            vals.append(max(d["sectioned_samples_per_s"], d["naive_samples_per_s"]))
-            detail = d
-    v = statistics.median(vals)
+            sec.append(Mr / ts)
+            nai.append(Mr / tn)
+    v_sec, v_nai = statistics.median(sec), statistics.median(nai)
+    v = max(v_sec, v_nai)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"reference CPU path (oracle/ C restatement of aliaskit): "
-                               f"psa_construct N={n_items:.0e} + sectioned (serial, S={a.section}) "
-                               f"and naive (<=16 workers) sampling of {n_samples:.0e} draws; "
-                               "value = the faster sampler",
-                   "build_items_per_s": detail["build_items_per_s"],
-                   "sectioned_samples_per_s": detail["sectioned_samples_per_s"],
-                   "naive_samples_per_s": detail["naive_samples_per_s"]},
+        "config": {"workload": f"reference CPU path (oracle/ C restatement of aliaskit) on the GPU arm's "
+                               f"workload: psa_construct of the same N={N:.0e} float32 uniform weights "
+                               f"(gen_uniform seed=1, bit-identical; upcast to f64), then per step "
+                               f"{Mr:.0e} sectioned (S={a.section}, serial) and {Mr:.0e} naive "
+                               f"(<=16 workers) draws from that table; value = the faster sampler",
+                   "n": N, "section_size": a.section, "draws_per_step_each": Mr,
+                   "same_config": {"build": True, "table": True,
+                                   "sampling": "same table and S, bounded draw count per step"},
+                   "build_items_per_s": N / t_build, "build_s": t_build,
+                   "sectioned_samples_per_s": v_sec, "naive_samples_per_s": v_nai,
+                   "cpu_model": cpu_model(), "nproc": threads},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"N={n_items:.0e} float32-upcast uniform weights, {n_samples:.0e} draws"},
+                         "sample": f"N={N:.0e} table (built once, {t_build:.1f} s), {Mr:.0e} draws "
+                                   f"per sampler per step; CPU {cpu_model()}"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -261,10 +320,18 @@ def run_ours(a):
 
     ev = lambda: torch.cuda.Event(enable_timing=True)
 
+    bcast_step = a.broadcast and world > 1
+
     def step(record):
         e0, e1, e2 = ev(), ev(), ev()
         e0.record()
-        ak.pack.build_table(ws, table)
+        if bcast_step:
+            # rank 0 builds, the table is replicated over NVLink (NCCL)
+            if rank == 0:
+                ak.pack.build_table(ws, table)
+            dist.broadcast(table.rows, 0)
+        else:
+            ak.pack.build_table(ws, table)
         e1.record()
         # host part of sectioned_sample (bit-exact binomial assignment) is
         # inside the sampling interval, as in the reference
@@ -328,17 +395,26 @@ def run_ours(a):
     t_plus = min(time_launch(lambda: ak.psa_plus_construct(ws), reps=1) for _ in range(5))
     torch.cuda.empty_cache()
 
-    traffic = None
+    # DRAM traffic comes from the committed ncu --set full capture of the same
+    # configuration (profiles/ncu_summary.json), not from this run (ncu
+    # replays kernels; a bench number is never taken under it)
+    traffic = b_traffic = None
+    traffic_src = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and dtype == torch.float32 and N == 10**9:
         try:
             with open(prof) as f:
                 ps = json.load(f)
-            k = ps.get("kernels", {}).get("k_sample_sectioned")
+            ks = ps.get("kernels", {})
+            k = ks.get("k_sample_sectioned")
             if k and k.get("dram_bytes") and k.get("draws"):
                 traffic = k["dram_bytes"] / k["draws"] * d0
+            bk = [v for kk, v in ks.items() if kk.startswith("k_build_")]
+            if bk:
+                b_traffic = sum(v["dram_bytes"] for v in bk)
+            traffic_src = "profiles/ncu_summary.json: " + ps.get("source", "ncu capture")
         except Exception:
-            traffic = None
+            traffic = b_traffic = None
 
     # end-to-end through the public API with host buffers (per rank): every
     # step copies the f32 weights in from pinned host memory, builds the table
@@ -347,13 +423,20 @@ def run_ours(a):
     # (copy-in of step i+1 and copy-out of step i-1 overlap step i's compute,
     # double-buffered), as a streaming user would run it; the time is the wall
     # clock of all steps including pipeline fill and drain, max over ranks.
-    e2e = None
-    if not a.no_e2e:
+    def run_e2e(out_dtype):
+        """End to end through the public API with host buffers (per rank):
+        every step copies the f32 weights in from pinned host memory, builds
+        the table (make_weight_set -> psa_construct), draws its samples and
+        copies them out to pinned host memory.  Steps are software-pipelined
+        over three streams (copy-in of step i+1 and copy-out of step i-1
+        overlap step i's compute, double-buffered), as a streaming user would
+        run it; the time is the wall clock of all steps including pipeline
+        fill and drain, max over ranks."""
         Me = int(a.e2e_samples)
         K = a.e2e_steps
-        cnt_e = Me  # per GPU (weak scaling, as the device-resident measurement)
+        ob = 8 if out_dtype == torch.int64 else 4
         w_host = ws.weights.cpu().pin_memory()
-        o_host = [torch.empty(max(cnt_e, 1), dtype=torch.int64).pin_memory() for _ in range(2)]
+        o_host = [torch.empty(max(Me, 1), dtype=out_dtype).pin_memory() for _ in range(2)]
         wd = [torch.empty_like(ws.weights) for _ in range(2)]
         s_in, s_cmp, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         ev_in = [torch.cuda.Event() for _ in range(K + 1)]
@@ -377,15 +460,14 @@ def run_ours(a):
                 te = ak.psa_construct(wse)
                 st_e = 7 + 64 * rank + i
                 asg_e = ak.assign_sections(N, S, Me, 1, st_e)
-                f_e, c_e, oo_e, dr_e = 0, asg_e.n_sections, 0, Me
                 cd = torch.from_numpy(asg_e.counts).to(dev, non_blocking=True)
                 odf = torch.from_numpy(np.concatenate([[0], np.cumsum(asg_e.counts)[:-1]])).to(dev, non_blocking=True)
-                if od[i % 2] is None or od[i % 2].numel() < max(dr_e, 1):
-                    od[i % 2] = torch.empty(max(dr_e, 1), dtype=torch.int64, device=dev)
-                sectioned_sample_into(te, asg_e.section_size, cd, odf, f_e, c_e, ak.RngStream(1, st_e),
-                                      od[i % 2], oo_e, rng_mode, n_out=dr_e)
+                if od[i % 2] is None:
+                    od[i % 2] = torch.empty(max(Me, 1), dtype=out_dtype, device=dev)
+                sectioned_sample_into(te, asg_e.section_size, cd, odf, 0, asg_e.n_sections, ak.RngStream(1, st_e),
+                                      od[i % 2], 0, rng_mode, n_out=Me)
                 ev_cmp[i].record(s_cmp)
-                return dr_e
+                return Me
 
         def copy_out(i, dr):
             with torch.cuda.stream(s_out):
@@ -411,11 +493,48 @@ def run_ours(a):
         if world > 1:
             dist.all_reduce(tt2, op=dist.ReduceOp.MAX)
         el = float(tt2.item())
-        e2e = {"value": Me * world * K / el, "unit": UNIT,
-               "h2d_bytes_per_step": int(N * b_w), "d2h_bytes_per_step": int(cnt_e * 8),
-               "path": "pinned host f32 weights -> make_weight_set -> psa_construct -> "
-                       "sectioned_sample -> pinned host int64 samples, 3-stream pipeline",
-               "samples_per_step": Me, "steps": K, "s_per_step": el / K}
+        del wd, od, o_host, w_host
+        torch.cuda.empty_cache()
+        return {"value": Me * world * K / el, "unit": UNIT,
+                "h2d_bytes_per_step": int(N * b_w), "d2h_bytes_per_step": int(Me * ob),
+                "path": f"pinned host {a.dtype} weights -> make_weight_set -> psa_construct -> "
+                        f"sectioned_sample -> pinned host {str(out_dtype)[6:]} samples, 3-stream pipeline",
+                "samples_per_step": Me, "steps": K, "s_per_step": el / K}
+
+    e2e = e2e_i32 = None
+    if not a.no_e2e:
+        e2e = run_e2e(torch.int64)
+        e2e_i32 = run_e2e(torch.int32)
+
+    # C5 as BASELINE.json states it: the float64 table (the reference's dtype)
+    f64 = None
+    if not a.no_f64 and dtype == torch.float32:
+        del out
+        torch.cuda.empty_cache()
+        ws64 = ak.gen_uniform(N, ak.RngStream(seed=1), dtype=torch.float64, device=dev)
+        t64 = ak.psa_construct(ws64)
+        tb64 = time_launch(lambda: ak.pack.build_table(ws64, t64), reps=3)
+        by64 = N * (2 * 8 + 16)
+        asg64 = ak.assign_sections(N, S, M, r0.seed, r0.stream)
+        c64 = torch.from_numpy(asg64.counts).to(dev)
+        o64 = torch.from_numpy(np.concatenate([[0], np.cumsum(asg64.counts)[:-1]])).to(dev)
+        out64 = torch.empty(d0, dtype=torch.int64, device=dev)
+        tp64 = time_launch(lambda: sectioned_sample_into(t64, asg64.section_size, c64, o64, f0, c0, r0, out64, o0,
+                                                         rng_mode, n_out=d0))
+        pb64 = d0 * 8 + c0 * S_eff * 16
+        f64 = {"build": {"items_per_s": N / tb64, "ms": tb64 * 1e3,
+                         "roofline": {"bound": "hbm", "achieved": by64 / tb64 / 1e9, "peak": peak,
+                                      "unit": "GB/s", "frac": by64 / tb64 / 1e9 / peak,
+                                      "algorithmic_bytes": by64, "bytes_per_item": 32, "traffic": None}},
+               "sampling": {"samples_per_s": d0 / tp64,
+                            "roofline": {"bound": "hbm", "achieved": pb64 / tp64 / 1e9, "peak": peak,
+                                         "unit": "GB/s", "frac": pb64 / tp64 / 1e9 / peak,
+                                         "algorithmic_bytes_per_launch": pb64,
+                                         "kernel": "k_sample_sectioned (f64 rows staged as threshold/alias arrays)"}},
+               "workload": f"C5 float64: N={N:.0e} gen_uniform(seed=1) float64 weights, 16-B rows; build best-of-3 "
+                           f"median, one sectioned pass ({d0} draws, {c0} sections of S={S_eff}, rng={rng_mode})"}
+        del ws64, t64, out64
+        torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -437,6 +556,12 @@ def run_ours(a):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": t_step / a.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "dtypes": {"weights": a.dtype,
+                       "table_rows": "f32 threshold + u32 alias (8 B)" if dtype == torch.float32
+                                     else "f64 threshold + u64 alias (16 B)",
+                       "arithmetic": "f64 (construction keys: double-double tile bases + f64 "
+                                     "in-tile prefixes; sampling rule in f64)",
+                       "samples": "int64 (e2e_int32: int32)"},
             "data": "synthetic",
             "config": {"workload": f"C4+C5: N={N:.0e} {a.dtype} table (gen_uniform seed=1) built per step, "
                                    f"then {M:.0e} sectioned draws per GPU (S={S}, RngStream(1, 7+rank), "
@@ -449,17 +574,24 @@ def run_ours(a):
             "build": {"items_per_s": N * a.steps / t_build, "ms": t_build / a.steps * 1e3,
                       "roofline": {"bound": "hbm", "achieved": bach, "peak": peak, "unit": "GB/s",
                                    "frac": bach / peak, "algorithmic_bytes": build_bytes,
-                                   "bytes_per_item": 2 * b_w + b_row}},
+                                   "bytes_per_item": 2 * b_w + b_row, "traffic": b_traffic,
+                                   "traffic_source": traffic_src if b_traffic else None,
+                                   "kernels": "k_build_scan + k_build_coarse + k_build_split + k_build_pack"}},
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                         "frac": ach / peak, "traffic": traffic, "kernel": "k_sample_sectioned",
+                         "frac": ach / peak, "traffic": traffic,
+                         "traffic_source": traffic_src if traffic else None, "kernel": "k_sample_sectioned",
                          "algorithmic_bytes_per_launch": pass_bytes, "peak_kind": peak_kind},
             "build_psa_plus": {"items_per_s": N / t_plus, "ms": t_plus * 1e3,
                                "frac": build_bytes / t_plus / 1e9 / peak},
             "sampling_reference_rng": {"samples_per_s": d0 / t_pass_ref,
                                        "frac": pass_bytes / t_pass_ref / 1e9 / peak},
             "e2e": e2e,
+            "e2e_int32": e2e_i32,
+            "c5_float64": f64,
             "cpu_baseline": cpu,
             "table_broadcast": bcast,
+            "step_variant": ("rank 0 builds, NCCL broadcast of the table every step" if bcast_step
+                             else "every rank rebuilds the table from its replicated weights"),
             "gpu_launches": a.steps * (4 + len(passes)),
             "clocks": clocks,
             "wall_s_timed_region": wall,

@@ -56,6 +56,10 @@ typedef enum {
 } ak_status;
 
 enum { AK_F32 = 0, AK_F64 = 1 };
+/* Sample index dtype: AK_I64 (int64, the reference's dtype, sample.py:116)
+ * or AK_I32 (opt-in, tables with n <= 2^31-1: half the output bytes, the
+ * same 1-based values) */
+enum { AK_I32 = 2, AK_I64 = 3 };
 enum { AK_RNG_REFERENCE = 0, /* Philox2x64-10 word 0, bit-exact with rng.py */
        AK_RNG_PHILOX4X32 = 1 /* GPU-native Philox4x32-10, two 53-bit draws per call */ };
 
@@ -193,6 +197,10 @@ int ak_residual_scatter(const void *res_rows, const int64_t *res_idx, uint64_t n
 int ak_sample_naive(const void *rows, int dtype, uint64_t n, double avg, uint64_t lo,
                     uint64_t span, uint64_t seed, uint64_t stream_id, uint64_t ctr0, uint64_t m,
                     int64_t *out, int rng_mode, void *stream);
+/* ak_sample_naive with the output index dtype chosen (AK_I64 / AK_I32). */
+int ak_sample_naive_out(const void *rows, int dtype, uint64_t n, double avg, uint64_t lo,
+                        uint64_t span, uint64_t seed, uint64_t stream_id, uint64_t ctr0, uint64_t m,
+                        void *out, int out_dtype, int rng_mode, void *stream);
 /* The bucket rule fed explicit f64 uniforms (tests/test_sample.py:20-25):
  * the "identical uniform variates -> identical indices" parity hook. */
 int ak_sample_from_uniforms(const void *rows, int dtype, uint64_t n, double avg, uint64_t lo,
@@ -214,6 +222,11 @@ int ak_sample_sectioned(const void *rows, int dtype, uint64_t n, double avg, uin
                         const int64_t *counts, const int64_t *offsets, uint64_t first,
                         uint64_t count, uint64_t seed, uint64_t stream_id, uint64_t ctr0,
                         int64_t *out, int64_t out_base, int rng_mode, void *stream);
+/* ak_sample_sectioned with the output index dtype chosen (AK_I64 / AK_I32). */
+int ak_sample_sectioned_out(const void *rows, int dtype, uint64_t n, double avg, uint64_t S,
+                            const int64_t *counts, const int64_t *offsets, uint64_t first,
+                            uint64_t count, uint64_t seed, uint64_t stream_id, uint64_t ctr0,
+                            void *out, int out_dtype, int64_t out_base, int rng_mode, void *stream);
 
 /* ---- verification / conversion ------------------------------------------ */
 

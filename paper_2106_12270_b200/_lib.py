@@ -19,6 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("AK_LIB_PATH") or os.path.join(_HERE, "libaliaskit_b200.so")
 
 F32, F64 = 0, 1
+I32, I64 = 2, 3  # sample index dtypes (ak_sample_*_out)
 RNG_REFERENCE, RNG_PHILOX4X32 = 0, 1
 RNG_MODES = {"reference": RNG_REFERENCE, "philox4x32": RNG_PHILOX4X32}
 
@@ -52,11 +53,14 @@ _SIGS = {
                                sz, vp]),
     "ak_residual_scatter": (ci, [vp, vp, u64, dbl, ci, vp, vp]),
     "ak_sample_naive": (ci, [vp, ci, u64, dbl, u64, u64, u64, u64, u64, u64, vp, ci, vp]),
+    "ak_sample_naive_out": (ci, [vp, ci, u64, dbl, u64, u64, u64, u64, u64, u64, vp, ci, ci, vp]),
     "ak_sample_from_uniforms": (ci, [vp, ci, u64, dbl, u64, u64, vp, u64, vp, vp]),
     "ak_num_sections": (u64, [u64, u64]),
     "ak_assign_subtree": (ci, [u64, u64, u64, u64, u64, u64, u64, vp]),
     "ak_sample_sectioned": (ci, [vp, ci, u64, dbl, u64, vp, vp, u64, u64, u64, u64, u64, vp, i64,
                                  ci, vp]),
+    "ak_sample_sectioned_out": (ci, [vp, ci, u64, dbl, u64, vp, vp, u64, u64, u64, u64, u64, vp,
+                                     ci, i64, ci, vp]),
     "ak_validate_workspace_bytes": (sz, [u64]),
     "ak_validate_table": (ci, [vp, ci, u64, vp, ci, dbl, dbl, vp, vp, vp, vp, sz, vp]),
     "ak_validate_table_range": (ci, [vp, ci, u64, u64, u64, vp, ci, dbl, dbl, vp, vp, vp, vp, sz, vp]),

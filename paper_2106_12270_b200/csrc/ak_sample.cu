@@ -69,10 +69,10 @@ __device__ __forceinline__ double ph4_single(u64 v, u64 strm, u64 seed)
 // ---------------------------------------------------------------------------
 // naive sampler (sample.py:73-84): one counter per draw, random row gather
 // ---------------------------------------------------------------------------
-template <typename RowT, int MODE>
+template <typename RowT, int MODE, typename OutT>
 __global__ void __launch_bounds__(256) k_sample_naive(const RowT *__restrict__ rows, double avg,
                                                       i64 lo, i64 span, u64 seed, u64 strm,
-                                                      u64 ctr0, u64 m, i64 *__restrict__ out)
+                                                      u64 ctr0, u64 m, OutT *__restrict__ out)
 {
     constexpr int U = 4;  // draws in flight per thread
     const u64 nthr = (u64)gridDim.x * blockDim.x;
@@ -98,8 +98,8 @@ __global__ void __launch_bounds__(256) k_sample_naive(const RowT *__restrict__ r
         for (int j = 0; j < U; ++j) {
             if (idx[j] < m) {
                 double x = u[j] * (double)span;
-                out[idx[j]] = ((x - (double)k[j]) * avg < (double)r[j].tw) ? (lo + k[j] + 1)
-                                                                              : (i64)r[j].alias;
+                out[idx[j]] = (OutT)(((x - (double)k[j]) * avg < (double)r[j].tw) ? (lo + k[j] + 1)
+                                                                                   : (i64)r[j].alias);
             }
         }
         (void)tid;
@@ -168,15 +168,26 @@ struct SoA64View {
 // lane t stores (d1 of t, d0 of t+1) as one vector and the warp's two end
 // elements with 8-byte stores.  v0/v1: whether each draw of the pair is in
 // range.  All lanes of the warp must call this (shuffles).
-__device__ __forceinline__ void store_pair(i64 *o0, i64 d0, i64 d1, bool v0, bool v1, int par,
+template <typename OutT> struct Pair2;
+template <> struct Pair2<i64> {
+    typedef longlong2 V;
+    static __device__ __forceinline__ V mk(i64 a, i64 b) { return make_longlong2(a, b); }
+};
+template <> struct Pair2<int32_t> {
+    typedef int2 V;
+    static __device__ __forceinline__ V mk(i64 a, i64 b) { return make_int2((int)a, (int)b); }
+};
+template <typename OutT>
+__device__ __forceinline__ void store_pair(OutT *o0, i64 d0, i64 d1, bool v0, bool v1, int par,
                                            int lane)
 {
+    typedef typename Pair2<OutT>::V V;
     if (par == 0) {
         if (v0 && v1) {
-            *reinterpret_cast<longlong2 *>(o0) = make_longlong2(d0, d1);
+            *reinterpret_cast<V *>(o0) = Pair2<OutT>::mk(d0, d1);
         } else {
-            if (v0) o0[0] = d0;
-            if (v1) o0[1] = d1;
+            if (v0) o0[0] = (OutT)d0;
+            if (v1) o0[1] = (OutT)d1;
         }
         return;
     }
@@ -184,9 +195,9 @@ __device__ __forceinline__ void store_pair(i64 *o0, i64 d0, i64 d1, bool v0, boo
     const bool nv = __shfl_down_sync(0xffffffffu, (int)v0, 1) != 0;
     const bool vec = lane < 31 && v1 && nv;
     const bool prev_vec = __shfl_up_sync(0xffffffffu, (int)vec, 1) != 0 && lane > 0;
-    if (vec) *reinterpret_cast<longlong2 *>(o0 + 1) = make_longlong2(d1, nx);
-    else if (v1) o0[1] = d1;
-    if (v0 && !prev_vec) o0[0] = d0;
+    if (vec) *reinterpret_cast<V *>(o0 + 1) = Pair2<OutT>::mk(d1, nx);
+    else if (v1) o0[1] = (OutT)d1;
+    if (v0 && !prev_vec) o0[0] = (OutT)d0;
 }
 
 // Philox4x32-10 with the round keys formed from the (warp-uniform) seed
@@ -289,17 +300,28 @@ __device__ __forceinline__ void store_fast(i64 *p, u32 d0, u32 d1, int lane)
         *reinterpret_cast<uint2 *>(p + 1) = make_uint2(d1, 0u);
     }
 }
+// int32 outputs (opt-in): one 8-byte store per aligned pair
+template <int PAR>
+__device__ __forceinline__ void store_fast(int32_t *p, u32 d0, u32 d1, int lane)
+{
+    if (PAR == 0) {
+        *reinterpret_cast<uint2 *>(p) = make_uint2(d0, d1);
+    } else {
+        reinterpret_cast<u32 *>(p)[0] = d0;
+        reinterpret_cast<u32 *>(p)[1] = d1;
+    }
+}
 
-template <int PAR, int U = 3>
+template <int PAR, typename OutT, int U = 3>
 __device__ __forceinline__ void fast_pairs_f32_p(const RowF32 *tab, u32 cl0, u32 ch, u64 strm,
-                                                 const Ph4Keys &rk, i64 *ob, u32 qa, u32 qb, int b,
+                                                 const Ph4Keys &rk, OutT *ob, u32 qa, u32 qb, int b,
                                                  u32 lo1, double avg, int lane)
 {
     const u32 sl = (u32)strm, sh = (u32)(strm >> 32);
     const int sk = 32 - b;
     const u64 fmask = (1ull << (53 - b)) - 1;
     const u32 step = blockDim.x;
-    i64 *p = ob + 2 * (u64)(qa + threadIdx.x);
+    OutT *p = ob + 2 * (u64)(qa + threadIdx.x);
     u32 q = qa + threadIdx.x;
     // U independent calls in flight per thread: the rounds are a serial
     // multiply-xor chain and 32 warps per SM alone leave it latency bound
@@ -320,12 +342,13 @@ __device__ __forceinline__ void fast_pairs_f32_p(const RowF32 *tab, u32 cl0, u32
     }
 }
 
+template <typename OutT>
 __device__ __forceinline__ void fast_pairs_f32(const RowF32 *tab, u32 cl0, u32 ch, u64 strm,
-                                               const Ph4Keys &rk, i64 *ob, u32 qa, u32 qb,
+                                               const Ph4Keys &rk, OutT *ob, u32 qa, u32 qb,
                                                int b, u32 lo1, double avg, int par, int lane)
 {
-    if (par) fast_pairs_f32_p<1>(tab, cl0, ch, strm, rk, ob, qa, qb, b, lo1, avg, lane);
-    else fast_pairs_f32_p<0>(tab, cl0, ch, strm, rk, ob, qa, qb, b, lo1, avg, lane);
+    if (par) fast_pairs_f32_p<1, OutT>(tab, cl0, ch, strm, rk, ob, qa, qb, b, lo1, avg, lane);
+    else fast_pairs_f32_p<0, OutT>(tab, cl0, ch, strm, rk, ob, qa, qb, b, lo1, avg, lane);
 }
 
 // The same interior loop for f64 tables staged in shared memory, either as
@@ -343,15 +366,15 @@ __device__ __forceinline__ u32 rule_f64_pow2(const V &tab, u32 wl, u32 wh, int s
     return (frac * avg < row.tw) ? lo1 + k : (u32)row.alias;
 }
 
-template <class V, int PAR, int U = 3>
+template <class V, int PAR, typename OutT, int U = 3>
 __device__ __forceinline__ void fast_pairs_f64_p(const V &tab, u32 cl0, u32 ch, u64 strm,
-                                                 const Ph4Keys &rk, i64 *ob, u32 qa, u32 qb, int b,
+                                                 const Ph4Keys &rk, OutT *ob, u32 qa, u32 qb, int b,
                                                  u32 lo1, double avg, int lane)
 {
     const u32 sl = (u32)strm, sh = (u32)(strm >> 32);
     const int sk = 32 - b;
     const u32 step = blockDim.x;
-    i64 *p = ob + 2 * (u64)(qa + threadIdx.x);
+    OutT *p = ob + 2 * (u64)(qa + threadIdx.x);
     u32 q = qa + threadIdx.x;
     for (; q + (U - 1) * step < qb; q += U * step, p += 2 * U * (u64)step) {
         uint4 c[U];
@@ -378,11 +401,11 @@ __device__ __forceinline__ void fast_pairs_f64_p(const V &tab, u32 cl0, u32 ch, 
 // consecutive draws per step (one Philox4x32-10 call in the fast mode) and
 // the warp writes them as 16-byte stores where aligned.  SMODE 0 reads rows from
 // global memory (sections too large for shared memory).
-template <typename RowT, int MODE, int SMODE>
+template <typename RowT, int MODE, int SMODE, typename OutT>
 __global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
     const RowT *__restrict__ rows, u64 n, double avg, u64 S, const i64 *__restrict__ counts,
     const i64 *__restrict__ offsets, u64 first, u64 count, u64 seed, u64 stream_id, u64 ctr0,
-    i64 *__restrict__ out, i64 out_base, const Ph4Keys rk)
+    OutT *__restrict__ out, i64 out_base, const Ph4Keys rk)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) u64 bar;
@@ -457,11 +480,11 @@ __global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
         }
         const RowT *tabp = SMODE == 1 ? srows : src;
         const u64 strm = ak_derive(seed, stream_id, j, AK_SALT_SECTION);
-        i64 *o = out + (oj - out_base);
+        OutT *o = out + (oj - out_base);
         // pairs: pair p holds draws (2p - poff, 2p - poff + 1).  The fast RNG
         // pairs draws on its call boundary (counter ctr0 + i even); the
-        // reference RNG pairs them on the 16-byte output boundary.
-        const int obit = (int)(((uintptr_t)o >> 3) & 1);
+        // reference RNG pairs them on the pair-aligned output boundary.
+        const int obit = (int)(((uintptr_t)o / sizeof(OutT)) & 1);
         const i64 poff = MODE == AK_RNG_REFERENCE ? (i64)obit : (i64)(ctr0 & 1);
         const int par = MODE == AK_RNG_REFERENCE ? 0 : (int)((obit + (int)poff) & 1);
         const i64 p0 = (ia + poff) >> 1, p1 = (ib - 1 + poff) >> 1;  // inclusive
@@ -509,19 +532,19 @@ __global__ void __launch_bounds__(1024, 1) k_sample_sectioned(
             if ((u64)(u32)cb + (u64)(qa + nfast) > 0xFFFFFFFFull) nfast = 0;
             if (nfast > 0) {
                 if (qa > 0) generic(p0, p0 + qa - 1);
-                i64 *ob = o + (2 * p0 - poff);
+                OutT *ob = o + (2 * p0 - poff);
                 const u32 fa = (u32)qa, fb = (u32)(qa + nfast), l1 = (u32)(lo + 1);
                 if constexpr (sizeof(RowT) == 8) {
                     fast_pairs_f32(reinterpret_cast<const RowF32 *>(tabp), (u32)cb, (u32)(cb >> 32),
                                    strm, rk, ob, fa, fb, bb, l1, avg, par, lane);
                 } else if constexpr (SMODE == 2) {
                     const SoA64View v{stw, sal};
-                    if (par) fast_pairs_f64_p<SoA64View, 1>(v, (u32)cb, (u32)(cb >> 32), strm, rk, ob, fa, fb, bb, l1, avg, lane);
-                    else fast_pairs_f64_p<SoA64View, 0>(v, (u32)cb, (u32)(cb >> 32), strm, rk, ob, fa, fb, bb, l1, avg, lane);
+                    if (par) fast_pairs_f64_p<SoA64View, 1, OutT>(v, (u32)cb, (u32)(cb >> 32), strm, rk, ob, fa, fb, bb, l1, avg, lane);
+                    else fast_pairs_f64_p<SoA64View, 0, OutT>(v, (u32)cb, (u32)(cb >> 32), strm, rk, ob, fa, fb, bb, l1, avg, lane);
                 } else {
                     const RowF64 *v = reinterpret_cast<const RowF64 *>(tabp);
-                    if (par) fast_pairs_f64_p<const RowF64 *, 1>(v, (u32)cb, (u32)(cb >> 32), strm, rk, ob, fa, fb, bb, l1, avg, lane);
-                    else fast_pairs_f64_p<const RowF64 *, 0>(v, (u32)cb, (u32)(cb >> 32), strm, rk, ob, fa, fb, bb, l1, avg, lane);
+                    if (par) fast_pairs_f64_p<const RowF64 *, 1, OutT>(v, (u32)cb, (u32)(cb >> 32), strm, rk, ob, fa, fb, bb, l1, avg, lane);
+                    else fast_pairs_f64_p<const RowF64 *, 0, OutT>(v, (u32)cb, (u32)(cb >> 32), strm, rk, ob, fa, fb, bb, l1, avg, lane);
                 }
                 if (qa + nfast < np) generic(p0 + qa + nfast, p1);
                 continue;
@@ -540,28 +563,28 @@ int grid_for(u64 work, int threads, int per_sm = 8)
     return (int)g;
 }
 
-template <typename RowT>
+template <typename RowT, typename OutT>
 int launch_naive(const void *rows, double avg, u64 lo, u64 span, u64 seed, u64 strm, u64 ctr0,
-                 u64 m, i64 *out, int mode, cudaStream_t st)
+                 u64 m, OutT *out, int mode, cudaStream_t st)
 {
     int g = grid_for((m + 3) / 4, 256, 16);
     if (mode == AK_RNG_REFERENCE)
-        k_sample_naive<RowT, AK_RNG_REFERENCE><<<g, 256, 0, st>>>(
+        k_sample_naive<RowT, AK_RNG_REFERENCE, OutT><<<g, 256, 0, st>>>(
             (const RowT *)rows, avg, (i64)lo, (i64)span, seed, strm, ctr0, m, out);
     else
-        k_sample_naive<RowT, AK_RNG_PHILOX4X32><<<g, 256, 0, st>>>(
+        k_sample_naive<RowT, AK_RNG_PHILOX4X32, OutT><<<g, 256, 0, st>>>(
             (const RowT *)rows, avg, (i64)lo, (i64)span, seed, strm, ctr0, m, out);
     AK_LAUNCH_CHECK("k_sample_naive");
     return AK_OK;
 }
 
-template <typename RowT, int MODE, int SMODE>
+template <typename RowT, int MODE, int SMODE, typename OutT>
 int launch_sectioned_t(const void *rows, u64 n, double avg, u64 S, const i64 *counts,
                        const i64 *offsets, u64 first, u64 count, u64 seed, u64 sid, u64 ctr0,
-                       i64 *out, i64 out_base, cudaStream_t st)
+                       OutT *out, i64 out_base, cudaStream_t st)
 {
     size_t smem = SMODE == 1 ? S * sizeof(RowT) : (SMODE == 2 ? S * 12 : 0);
-    auto kern = k_sample_sectioned<RowT, MODE, SMODE>;
+    auto kern = k_sample_sectioned<RowT, MODE, SMODE, OutT>;
     if (SMODE) AK_SMEM_ATTR(kern, (int)smem);
     int per_sm = SMODE ? (smem > 110 * 1024 ? 1 : 2) : 2;
     u64 g = (u64)ak_num_sms() * per_sm;
@@ -571,31 +594,56 @@ int launch_sectioned_t(const void *rows, u64 n, double avg, u64 S, const i64 *co
     return AK_OK;
 }
 
-template <typename RowT, int MODE>
+template <typename RowT, int MODE, typename OutT>
 int launch_sectioned_m(const void *rows, u64 n, double avg, u64 S, const i64 *counts,
                        const i64 *offsets, u64 first, u64 count, u64 seed, u64 sid, u64 ctr0,
-                       i64 *out, i64 out_base, cudaStream_t st)
+                       OutT *out, i64 out_base, cudaStream_t st)
 {
     if (S * sizeof(RowT) <= 200 * 1024)
-        return launch_sectioned_t<RowT, MODE, 1>(rows, n, avg, S, counts, offsets, first, count,
-                                                 seed, sid, ctr0, out, out_base, st);
+        return launch_sectioned_t<RowT, MODE, 1, OutT>(rows, n, avg, S, counts, offsets, first,
+                                                       count, seed, sid, ctr0, out, out_base, st);
     if (sizeof(RowT) == 16 && S * 12 <= 200 * 1024 && n < 0xFFFFFFFFull)
-        return launch_sectioned_t<RowT, MODE, 2>(rows, n, avg, S, counts, offsets, first, count,
-                                                 seed, sid, ctr0, out, out_base, st);
-    return launch_sectioned_t<RowT, MODE, 0>(rows, n, avg, S, counts, offsets, first, count, seed,
-                                             sid, ctr0, out, out_base, st);
+        return launch_sectioned_t<RowT, MODE, 2, OutT>(rows, n, avg, S, counts, offsets, first,
+                                                       count, seed, sid, ctr0, out, out_base, st);
+    return launch_sectioned_t<RowT, MODE, 0, OutT>(rows, n, avg, S, counts, offsets, first, count,
+                                                   seed, sid, ctr0, out, out_base, st);
 }
 
-template <typename RowT>
+template <typename RowT, typename OutT>
 int launch_sectioned(const void *rows, u64 n, double avg, u64 S, const i64 *counts,
                      const i64 *offsets, u64 first, u64 count, u64 seed, u64 sid, u64 ctr0,
-                     i64 *out, i64 out_base, int mode, cudaStream_t st)
+                     OutT *out, i64 out_base, int mode, cudaStream_t st)
 {
     if (mode == AK_RNG_REFERENCE)
-        return launch_sectioned_m<RowT, AK_RNG_REFERENCE>(rows, n, avg, S, counts, offsets, first,
-                                                          count, seed, sid, ctr0, out, out_base, st);
-    return launch_sectioned_m<RowT, AK_RNG_PHILOX4X32>(rows, n, avg, S, counts, offsets, first,
-                                                       count, seed, sid, ctr0, out, out_base, st);
+        return launch_sectioned_m<RowT, AK_RNG_REFERENCE, OutT>(rows, n, avg, S, counts, offsets,
+                                                                first, count, seed, sid, ctr0, out,
+                                                                out_base, st);
+    return launch_sectioned_m<RowT, AK_RNG_PHILOX4X32, OutT>(rows, n, avg, S, counts, offsets,
+                                                             first, count, seed, sid, ctr0, out,
+                                                             out_base, st);
+}
+
+template <typename OutT>
+int naive_rows(const void *rows, int dtype, double avg, u64 lo, u64 span, u64 seed, u64 sid,
+               u64 ctr0, u64 m, OutT *out, int mode, cudaStream_t st)
+{
+    if (dtype == AK_F32) return launch_naive<RowF32, OutT>(rows, avg, lo, span, seed, sid, ctr0, m, out, mode, st);
+    if (dtype == AK_F64) return launch_naive<RowF64, OutT>(rows, avg, lo, span, seed, sid, ctr0, m, out, mode, st);
+    return AK_ERR_VALUE;
+}
+
+template <typename OutT>
+int sectioned_rows(const void *rows, int dtype, u64 n, double avg, u64 S, const i64 *counts,
+                   const i64 *offsets, u64 first, u64 count, u64 seed, u64 sid, u64 ctr0,
+                   OutT *out, i64 out_base, int mode, cudaStream_t st)
+{
+    if (dtype == AK_F32)
+        return launch_sectioned<RowF32, OutT>(rows, n, avg, S, counts, offsets, first, count, seed,
+                                              sid, ctr0, out, out_base, mode, st);
+    if (dtype == AK_F64)
+        return launch_sectioned<RowF64, OutT>(rows, n, avg, S, counts, offsets, first, count, seed,
+                                              sid, ctr0, out, out_base, mode, st);
+    return AK_ERR_VALUE;
 }
 
 }  // namespace
@@ -630,20 +678,30 @@ int ak_philox2x64(const uint64_t *ctr, const uint64_t *strm, const uint64_t *key
     return AK_OK;
 }
 
-int ak_sample_naive(const void *rows, int dtype, uint64_t n, double avg, uint64_t lo,
-                    uint64_t span, uint64_t seed, uint64_t stream_id, uint64_t ctr0, uint64_t m,
-                    int64_t *out, int rng_mode, void *stream)
+int ak_sample_naive_out(const void *rows, int dtype, uint64_t n, double avg, uint64_t lo,
+                        uint64_t span, uint64_t seed, uint64_t stream_id, uint64_t ctr0, uint64_t m,
+                        void *out, int out_dtype, int rng_mode, void *stream)
 {
     if (m == 0) return AK_OK;
     if (span == 0 || lo + span > n) return AK_ERR_VALUE;
     if (rng_mode != AK_RNG_REFERENCE && rng_mode != AK_RNG_PHILOX4X32) return AK_ERR_VALUE;
-    if (dtype == AK_F32)
-        return launch_naive<RowF32>(rows, avg, lo, span, seed, stream_id, ctr0, m, out, rng_mode,
-                                    ak_stream(stream));
-    if (dtype == AK_F64)
-        return launch_naive<RowF64>(rows, avg, lo, span, seed, stream_id, ctr0, m, out, rng_mode,
-                                    ak_stream(stream));
+    if (dtype != AK_F32 && dtype != AK_F64) return AK_ERR_VALUE;
+    cudaStream_t st = ak_stream(stream);
+    if (out_dtype == AK_I64)
+        return naive_rows<i64>(rows, dtype, avg, lo, span, seed, stream_id, ctr0, m, (i64 *)out,
+                               rng_mode, st);
+    if (out_dtype == AK_I32 && n <= 0x7FFFFFFFull)
+        return naive_rows<int32_t>(rows, dtype, avg, lo, span, seed, stream_id, ctr0, m,
+                                   (int32_t *)out, rng_mode, st);
     return AK_ERR_VALUE;
+}
+
+int ak_sample_naive(const void *rows, int dtype, uint64_t n, double avg, uint64_t lo,
+                    uint64_t span, uint64_t seed, uint64_t stream_id, uint64_t ctr0, uint64_t m,
+                    int64_t *out, int rng_mode, void *stream)
+{
+    return ak_sample_naive_out(rows, dtype, n, avg, lo, span, seed, stream_id, ctr0, m, out, AK_I64,
+                               rng_mode, stream);
 }
 
 int ak_sample_from_uniforms(const void *rows, int dtype, uint64_t n, double avg, uint64_t lo,
@@ -665,25 +723,34 @@ int ak_sample_from_uniforms(const void *rows, int dtype, uint64_t n, double avg,
     return AK_OK;
 }
 
-int ak_sample_sectioned(const void *rows, int dtype, uint64_t n, double avg, uint64_t S,
-                        const int64_t *counts, const int64_t *offsets, uint64_t first,
-                        uint64_t count, uint64_t seed, uint64_t stream_id, uint64_t ctr0,
-                        int64_t *out, int64_t out_base, int rng_mode, void *stream)
+int ak_sample_sectioned_out(const void *rows, int dtype, uint64_t n, double avg, uint64_t S,
+                            const int64_t *counts, const int64_t *offsets, uint64_t first,
+                            uint64_t count, uint64_t seed, uint64_t stream_id, uint64_t ctr0,
+                            void *out, int out_dtype, int64_t out_base, int rng_mode, void *stream)
 {
     if (count == 0) return AK_OK;
     if (S < 1) return AK_ERR_INVALID_SECTION_SIZE;
     if (S > n) S = n;
     if (first + count > ak_num_sections(n, S)) return AK_ERR_VALUE;
     if (rng_mode != AK_RNG_REFERENCE && rng_mode != AK_RNG_PHILOX4X32) return AK_ERR_VALUE;
-    if (dtype == AK_F32)
-        return launch_sectioned<RowF32>(rows, n, avg, S, counts, offsets, first, count, seed,
-                                        stream_id, ctr0, out, out_base, rng_mode,
-                                        ak_stream(stream));
-    if (dtype == AK_F64)
-        return launch_sectioned<RowF64>(rows, n, avg, S, counts, offsets, first, count, seed,
-                                        stream_id, ctr0, out, out_base, rng_mode,
-                                        ak_stream(stream));
+    if (dtype != AK_F32 && dtype != AK_F64) return AK_ERR_VALUE;
+    cudaStream_t st = ak_stream(stream);
+    if (out_dtype == AK_I64)
+        return sectioned_rows<i64>(rows, dtype, n, avg, S, counts, offsets, first, count, seed,
+                                   stream_id, ctr0, (i64 *)out, out_base, rng_mode, st);
+    if (out_dtype == AK_I32 && n <= 0x7FFFFFFFull)
+        return sectioned_rows<int32_t>(rows, dtype, n, avg, S, counts, offsets, first, count, seed,
+                                       stream_id, ctr0, (int32_t *)out, out_base, rng_mode, st);
     return AK_ERR_VALUE;
+}
+
+int ak_sample_sectioned(const void *rows, int dtype, uint64_t n, double avg, uint64_t S,
+                        const int64_t *counts, const int64_t *offsets, uint64_t first,
+                        uint64_t count, uint64_t seed, uint64_t stream_id, uint64_t ctr0,
+                        int64_t *out, int64_t out_base, int rng_mode, void *stream)
+{
+    return ak_sample_sectioned_out(rows, dtype, n, avg, S, counts, offsets, first, count, seed,
+                                   stream_id, ctr0, out, AK_I64, out_base, rng_mode, stream);
 }
 
 }  // extern "C"

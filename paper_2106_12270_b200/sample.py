@@ -58,20 +58,34 @@ def _rng_code(rng: str) -> int:
         raise ValueError(f"unknown rng mode {rng!r}: expected one of {sorted(_lib.RNG_MODES)}")
 
 
-def _check_out(out: torch.Tensor, need: int, dev: torch.device, what: str) -> None:
-    """A caller-supplied output buffer must be a contiguous int64 tensor on the
-    table's device with room for every draw the kernel writes through its raw
-    pointer; anything else raises instead of writing out of bounds."""
+def _check_out(out: torch.Tensor, need: int, dev: torch.device, what: str, n_rows: int = 0) -> None:
+    """A caller-supplied output buffer must be a contiguous int64 (or, for
+    tables of at most 2^31-1 rows, int32) tensor on the table's device with
+    room for every draw the kernel writes through its raw pointer; anything
+    else raises instead of writing out of bounds."""
     if not isinstance(out, torch.Tensor):
         raise TypeError(f"{what}: out must be a torch.Tensor")
-    if out.dtype != torch.int64:
-        raise ValueError(f"{what}: out must be int64, got {out.dtype}")
+    if out.dtype not in (torch.int64, torch.int32):
+        raise ValueError(f"{what}: out must be int64 (or int32), got {out.dtype}")
+    if out.dtype == torch.int32 and n_rows > 0x7FFFFFFF:
+        raise ValueError(f"{what}: int32 output needs n <= 2^31-1, the table has {n_rows} rows")
     if out.device != dev:
         raise ValueError(f"{what}: out is on {out.device}, the table on {dev}")
     if not out.is_contiguous():
         raise ValueError(f"{what}: out must be contiguous")
     if out.numel() < need:
         raise ValueError(f"{what}: out holds {out.numel()} draws, {need} are written")
+
+
+def _out_code(out: torch.Tensor) -> int:
+    return _lib.I32 if out.dtype == torch.int32 else _lib.I64
+
+
+def _new_out(m: int, dev: torch.device, out_dtype) -> torch.Tensor:
+    dt = torch.int64 if out_dtype is None else out_dtype
+    if dt not in (torch.int64, torch.int32):
+        raise ValueError(f"out_dtype must be torch.int64 or torch.int32, got {dt}")
+    return torch.empty(m, dtype=dt, device=dev)
 
 
 def sample_one(t: AliasTable, r: RngStream) -> int:
@@ -88,24 +102,24 @@ def sample_one(t: AliasTable, r: RngStream) -> int:
 
 
 def sample_batch(t: AliasTable, m: int, r: RngStream, workers: int = 1, rng: str = "reference",
-                 out: torch.Tensor | None = None) -> torch.Tensor:
+                 out: torch.Tensor | None = None, out_dtype: torch.dtype | None = None) -> torch.Tensor:
     """m independent draws (1-based item ids, device int64); advances r by m.
 
     ``workers`` is accepted for API parity; the output never depends on it
-    (sample.py:131-147), as on the reference.
+    (sample.py:131-147), as on the reference.  ``out_dtype=torch.int32``
+    (tables of at most 2^31-1 rows) writes the same ids as int32.
     """
     if m < 0:
         raise ValueError("sample count must be non-negative")
     dev = t.rows.device
     if out is None:
-        out = torch.empty(m, dtype=torch.int64, device=dev)
-    else:
-        _check_out(out, m, dev, "sample_batch")
+        out = _new_out(m, dev, out_dtype)
+    _check_out(out, m, dev, "sample_batch", t.n)
     with torch.cuda.device(dev):
-        _lib.check(_lib.lib().ak_sample_naive(
+        _lib.check(_lib.lib().ak_sample_naive_out(
             _lib.ptr(t.rows), t.dtype_code, t.n, t.average, 0, t.n, r.seed, r.stream,
-            r.counter & MASK64, m, _lib.ptr(out), _rng_code(rng), _lib.stream_ptr(dev)),
-            "sample_batch")
+            r.counter & MASK64, m, _lib.ptr(out), _out_code(out), _rng_code(rng),
+            _lib.stream_ptr(dev)), "sample_batch")
     r.counter += m
     return out
 
@@ -180,26 +194,28 @@ def sectioned_sample_into(t: AliasTable, S_eff: int, counts_d: torch.Tensor,
     if n_out is None:
         last = first + count - 1
         n_out = int((offsets_d[last] + counts_d[last]).item()) - out_base
-    _check_out(out, n_out, dev, "sectioned_sample")
+    _check_out(out, n_out, dev, "sectioned_sample", t.n)
     with torch.cuda.device(dev):
-        _lib.check(_lib.lib().ak_sample_sectioned(
+        _lib.check(_lib.lib().ak_sample_sectioned_out(
             _lib.ptr(t.rows), t.dtype_code, t.n, t.average, S_eff, _lib.ptr(counts_d),
             _lib.ptr(offsets_d), first, count, r.seed, r.stream, r.counter & MASK64,
-            _lib.ptr(out), out_base, _rng_code(rng), _lib.stream_ptr(dev)), "sectioned_sample")
+            _lib.ptr(out), _out_code(out), out_base, _rng_code(rng), _lib.stream_ptr(dev)),
+            "sectioned_sample")
 
 
 def sectioned_sample(t: AliasTable, S: int, M: int, r: RngStream, rng: str = "reference",
-                     out: torch.Tensor | None = None) -> torch.Tensor:
+                     out: torch.Tensor | None = None,
+                     out_dtype: torch.dtype | None = None) -> torch.Tensor:
     """M draws confined section by section to contiguous row ranges
-    (sample.py:243-267); section-major output; advances r by M."""
+    (sample.py:243-267); section-major output; advances r by M.
+    ``out_dtype=torch.int32`` (n <= 2^31-1) writes the same ids as int32."""
     if M < 0:
         raise ValueError("sample count must be non-negative")
     asg = assign_sections(t.n, S, M, r.seed, r.stream)
     dev = t.rows.device
     if out is None:
-        out = torch.empty(M, dtype=torch.int64, device=dev)
-    else:
-        _check_out(out, M, dev, "sectioned_sample")
+        out = _new_out(M, dev, out_dtype)
+    _check_out(out, M, dev, "sectioned_sample", t.n)
     if M:
         counts = torch.from_numpy(asg.counts).to(dev)
         offsets = torch.from_numpy(np.concatenate([[0], np.cumsum(asg.counts)[:-1]])).to(dev)

@@ -23,9 +23,12 @@ def run(args, timeout):
 
 
 def test_reference_arm_contract():
-    d = run(["--impl", "reference", "--steps", "1", "--warmup", "0", "--cpu-n", "1e5",
-             "--cpu-samples", "1e5"], 300)
+    d = run(["--impl", "reference", "--steps", "1", "--warmup", "0", "--n", "1e5",
+             "--ref-samples", "1e5"], 300)
     assert KEYS <= set(d) and d["impl"] == "reference"
+    c = d["config"]
+    assert c["n"] == 100_000 and c["same_config"]["build"] is True and c["nproc"] >= 1
+    assert c["sectioned_samples_per_s"] > 0 and c["naive_samples_per_s"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "port"
     assert d["value"] > 0 and d["higher_is_better"] is True
 
@@ -35,8 +38,11 @@ def test_our_arm_contract():
     d = run(["--steps", "1", "--warmup", "1", "--n", "1e6", "--samples", "1e8", "--no-cpu",
              "--e2e-samples", "1e7", "--e2e-steps", "1"], 600)
     assert KEYS <= set(d)
-    for k in ("roofline", "clocks", "gpu_launches", "build", "build_psa_plus"):
+    for k in ("roofline", "clocks", "gpu_launches", "build", "build_psa_plus", "e2e_int32",
+              "c5_float64", "dtypes"):
         assert k in d
+    assert d["e2e_int32"]["d2h_bytes_per_step"] * 2 == d["e2e"]["d2h_bytes_per_step"]
+    assert 0 < d["c5_float64"]["build"]["roofline"]["frac"] < 1.5
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0

@@ -242,7 +242,7 @@ def test_out_buffer_is_checked():
     t = ak.psa_construct(ak.make_weight_set(np.arange(1.0, 101.0)))
     r = ak.RngStream(1)
     for bad in (torch.empty(9, dtype=torch.int64, device=DEV),             # too short
-                torch.empty(10, dtype=torch.int32, device=DEV),            # wrong dtype
+                torch.empty(10, dtype=torch.int16, device=DEV),            # wrong dtype
                 torch.empty(20, dtype=torch.int64, device=DEV)[::2],       # strided
                 torch.empty(10, dtype=torch.int64)):                       # host
         with pytest.raises(ValueError):
@@ -335,3 +335,36 @@ def test_fast_rng_sectioned_bit_exact(ctr0, dtype, S, tail):
         sectioned_sample_into(t, S, counts, offs, first, count, ak.RngStream(seed, stream, ctr0),
                               buf[1:], 0, "philox4x32")
     assert np.array_equal(buf[1:].cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("rng_mode", ["reference", "philox4x32"])
+def test_int32_outputs_equal_int64(dtype, rng_mode):
+    """out_dtype=torch.int32 (opt-in, n <= 2^31-1) writes the int64 ids
+    narrowed: both samplers, both RNG modes, f32/f64 tables, fast interior and
+    generic edges (section size 2^12 pow2 and 1000 non-pow2), aligned and
+    misaligned output offsets."""
+    g = np.random.default_rng(32)
+    w = g.pareto(1.1, 300_000) + 1e-6
+    t = ak.psa_construct(ak.make_weight_set(torch.tensor(w, dtype=dtype)))
+    for ctr in (0, 1, 2**33 + 5):
+        a = ak.sample_batch(t, 100_003, ak.RngStream(5, 1, ctr), rng=rng_mode)
+        b = ak.sample_batch(t, 100_003, ak.RngStream(5, 1, ctr), rng=rng_mode, out_dtype=torch.int32)
+        assert b.dtype == torch.int32 and torch.equal(a, b.long())
+        for S in (1 << 12, 1000):
+            a = ak.sectioned_sample(t, S, 1_000_001, ak.RngStream(5, 2, ctr), rng=rng_mode)
+            b = ak.sectioned_sample(t, S, 1_000_001, ak.RngStream(5, 2, ctr), rng=rng_mode,
+                                    out_dtype=torch.int32)
+            assert b.dtype == torch.int32 and torch.equal(a, b.long())
+    # a misaligned int32 destination (odd element offset) through the pass API
+    asg = ak.assign_sections(t.n, 1 << 12, 500_000, 9, 4)
+    cd = torch.from_numpy(asg.counts).to(DEV)
+    od = torch.from_numpy(np.concatenate([[0], np.cumsum(asg.counts)[:-1]])).to(DEV)
+    from paper_2106_12270_b200.sample import sectioned_sample_into
+    ref = torch.empty(500_000, dtype=torch.int64, device=DEV)
+    sectioned_sample_into(t, asg.section_size, cd, od, 0, asg.n_sections, ak.RngStream(9, 4), ref, 0,
+                          rng_mode, n_out=500_000)
+    buf = torch.zeros(500_001, dtype=torch.int32, device=DEV)
+    sectioned_sample_into(t, asg.section_size, cd, od, 0, asg.n_sections, ak.RngStream(9, 4), buf[1:], 0,
+                          rng_mode, n_out=500_000)
+    assert torch.equal(buf[1:].long(), ref) and buf[0].item() == 0
