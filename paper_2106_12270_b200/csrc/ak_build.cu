@@ -312,9 +312,14 @@ __device__ __forceinline__ double sum8(const double x[8])
 }
 
 constexpr int SC_WARPS = 4;  // warps per scan CTA; each owns SUPER / SC_WARPS tiles
+constexpr int RS = 4;        // TMA ring slots per scan warp (half a tile in flight)
 template <typename T> struct ScanBuf {
-    // per warp a ring of NW chunk slots (chunk c of successive tiles in slot c)
-    static constexpr size_t BYTES = (size_t)SC_WARPS * NW * CH * sizeof(T);
+    // per warp a ring of NW chunk slots (chunk c of successive tiles in slot c),
+    // then the per-lane class sums of the warp's current tile ([2][NW][32]
+    // doubles: staged here instead of 32 registers, which held the scan at
+    // 19.7% occupancy)
+    static constexpr size_t RING = (size_t)SC_WARPS * RS * CH * sizeof(T);
+    static constexpr size_t BYTES = RING + (size_t)SC_WARPS * 2 * NW * 32 * sizeof(double);
 };
 
 // One pass over the weights.  Each warp streams its tiles chunk by chunk
@@ -331,7 +336,7 @@ __global__ void __launch_bounds__(SC_WARPS * 32) k_build_scan(const T *__restric
                                                               double avg, BuildWs W)
 {
     extern __shared__ __align__(128) unsigned char scan_smem[];
-    __shared__ __align__(8) u64 bars[SC_WARPS][NW];
+    __shared__ __align__(8) u64 bars[SC_WARPS][RS];
     __shared__ double s_tD[SUPER], s_tE[SUPER];
     __shared__ u32 s_tL[SUPER];
     __shared__ u64 s_fH[SUPER];
@@ -340,30 +345,31 @@ __global__ void __launch_bounds__(SC_WARPS * 32) k_build_scan(const T *__restric
     if (threadIdx.x == 0) s_st = atomicAdd(W.counter, 1u);
     if (lane == 0) {
 #pragma unroll
-        for (int c = 0; c < NW; ++c) mbar_init(&bars[wid][c], 1);
+        for (int c = 0; c < RS; ++c) mbar_init(&bars[wid][c], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     const u64 st = s_st;
     const u64 t0 = st * W.super;
     const u64 tn = (t0 + W.super <= W.nt) ? W.super : W.nt - t0;
-    T *ring = reinterpret_cast<T *>(scan_smem) + (size_t)wid * NW * CH;
+    T *ring = reinterpret_cast<T *>(scan_smem) + (size_t)wid * RS * CH;
     const T avgT = avg_floor<T>(avg);
     auto full_chunk = [&](u64 g) { return (g + 1) * CH <= n; };
-    auto issue = [&](u64 j, int c) {  // chunk c of the super-tile's tile j into slot c
+    auto issue = [&](u64 j, int c) {  // chunk c of the super-tile's tile j into slot c % RS
         const u64 g = (t0 + j) * NW + c;
+        const int sl = c & (RS - 1);
         if (lane == 0 && j < tn && full_chunk(g)) {
-            mbar_expect_tx(&bars[wid][c], CH * sizeof(T));
-            bulk_g2s(ring + c * CH, w + g * CH, CH * sizeof(T), &bars[wid][c]);
+            mbar_expect_tx(&bars[wid][sl], CH * sizeof(T));
+            bulk_g2s(ring + sl * CH, w + g * CH, CH * sizeof(T), &bars[wid][sl]);
         }
     };
 #pragma unroll
-    for (int c = 0; c < NW; ++c) issue((u64)wid, c);
-    u32 phase = 0;  // all slots complete once per tile: one parity for all
+    for (int c = 0; c < RS; ++c) issue((u64)wid, c);
+    u32 phase = 0;  // per-slot parity bits (a slot completes twice per tile)
 
     for (u64 j = wid; j < tn; j += SC_WARPS) {
         const u64 t = t0 + j;
-        double sD[NW], sE[NW];
+        double *ssum = reinterpret_cast<double *>(scan_smem + ScanBuf<T>::RING) + (size_t)wid * 2 * NW * 32;
         u32 cl = 0;
         unsigned char cf = NOFH;
 #pragma unroll
@@ -372,9 +378,11 @@ __global__ void __launch_bounds__(SC_WARPS * 32) k_build_scan(const T *__restric
             double xl[VV], xh[VV];
             u32 lm = 0, vm = 0;
             if (full_chunk(g)) {
-                mbar_wait(&bars[wid][c], phase);
+                const int sl = c & (RS - 1);
+                mbar_wait(&bars[wid][sl], (phase >> sl) & 1);
+                phase ^= 1u << sl;
                 T v[VV];
-                lds8_raw(ring + c * CH + lane * VV, v);
+                lds8_raw(ring + sl * CH + lane * VV, v);
 #pragma unroll
                 for (int q = 0; q < VV; ++q) {
                     const bool li = v[q] <= avgT;
@@ -385,10 +393,12 @@ __global__ void __launch_bounds__(SC_WARPS * 32) k_build_scan(const T *__restric
                 }
                 vm = 0xFFu;
                 // the slot's reads are done (values consumed) and ordered
-                // before the async-proxy refill of the next tile's chunk c
+                // before the async-proxy refill: chunk c + RS of this tile or
+                // chunk c + RS - NW of the warp's next tile
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
-                issue(j + SC_WARPS, c);
+                if (c + RS < NW) issue(j, c + RS);
+                else issue(j + SC_WARPS, c + RS - NW);
             } else {
                 double v[VV];
                 load8(w, n, g * CH + (u64)lane * VV, v);
@@ -405,8 +415,8 @@ __global__ void __launch_bounds__(SC_WARPS * 32) k_build_scan(const T *__restric
             const u32 hm = vm & ~lm;
             const int nlq = __popc(lm), nhq = __popc(hm);
             (void)nhq;
-            sD[c] = sum8(xl);
-            sE[c] = sum8(xh);
+            ssum[c * 32 + lane] = sum8(xl);
+            ssum[(NW + c) * 32 + lane] = sum8(xh);
             const u32 nl = __reduce_add_sync(0xffffffffu, (u32)nlq);
             const unsigned char fh = first_item(hm, lane);
             if (lane == c) {
@@ -414,9 +424,23 @@ __global__ void __launch_bounds__(SC_WARPS * 32) k_build_scan(const T *__restric
                 cf = fh;
             }
         }
-        phase ^= 1;
         // chunk totals -> lanes 0..7, then their monotone scan -> chunk bounds
-        const double rD = reduce8(sD, lane), rE = reduce8(sE, lane);
+        // chunk totals: lane l sums lanes 8q..8q+7 of chunk l>>2 (q = l&3)
+        // for both classes, two butterfly steps finish: lanes 4c..4c+3 hold
+        // chunk c's totals (the reduce-scatter layout of reduce8)
+        __syncwarp();
+        double rD, rE;
+        {
+            const int cc = lane >> 2, qq = lane & 3;
+            const double *pD = ssum + cc * 32 + qq * 8, *pE = ssum + (NW + cc) * 32 + qq * 8;
+            rD = sum8(pD);
+            rE = sum8(pE);
+            rD = rD + __shfl_xor_sync(0xffffffffu, rD, 1);
+            rE = rE + __shfl_xor_sync(0xffffffffu, rE, 1);
+            rD = rD + __shfl_xor_sync(0xffffffffu, rD, 2);
+            rE = rE + __shfl_xor_sync(0xffffffffu, rE, 2);
+        }
+        __syncwarp();  // ssum reads done before the next tile's writes
         double x = __shfl_sync(0xffffffffu, rD, (lane & 7) * 4), y = __shfl_sync(0xffffffffu, rE, (lane & 7) * 4);
         x = x > 0.0 ? x : 0.0;  // a class's chunk total is a sum of non-negative terms
         y = y > 0.0 ? y : 0.0;
