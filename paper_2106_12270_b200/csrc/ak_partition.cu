@@ -319,7 +319,8 @@ template <typename T>
 __global__ void __launch_bounds__(PLAN_RUN) k_plan_batched(PlanArgs A, const T *__restrict__ h_w)
 {
     __shared__ i64 ends[2];
-    extern __shared__ double stage[];
+    __shared__ __align__(8) u64 bar;
+    extern __shared__ __align__(16) double stage[];
     const u64 i0 = 1 + (u64)blockIdx.x * PLAN_RUN;
     if (i0 >= A.s) return;
     u64 i1 = i0 + PLAN_RUN - 1;  // inclusive
@@ -348,10 +349,38 @@ __global__ void __launch_bounds__(PLAN_RUN) k_plan_batched(PlanArgs A, const T *
     const i64 l0 = nA - hB > 0 ? nA - hB : 0;
     const i64 l1 = nB - hA < A.nl ? nB - hA : A.nl;
     const i64 llen = l1 - l0 + 1;
-    const bool staged = hlen > 0 && llen > 0 && hlen + llen <= PLAN_SMEM_DOUBLES;
-    if (staged) {
-        for (i64 t = threadIdx.x; t < hlen; t += blockDim.x) stage[t] = A.hpre[hA + t];
-        for (i64 t = threadIdx.x; t < llen; t += blockDim.x) stage[hlen + t] = A.lpre[l0 + t];
+    // the windows are staged with 1-D bulk async copies (the TMA engine) at
+    // 16-byte-congruent offsets: H window at stage[k - hA2], L window at
+    // stage[lbase + k - l02] (hA2, l02 = the window starts rounded down to
+    // even); the odd end elements a bulk copy cannot cover are plain loads
+    const i64 hA2 = hA & ~(i64)1, l02 = l0 & ~(i64)1;
+    const i64 lbase = (hB - hA2 + 2) & ~(i64)1;
+    const bool staged = hlen > 0 && llen > 0 && lbase + (l1 - l02 + 2) <= PLAN_SMEM_DOUBLES;
+    const bool tma = ((((uintptr_t)A.hpre) | ((uintptr_t)A.lpre)) & 15) == 0;
+    if (staged && tma) {
+        // bulk parts: the even-aligned interiors [c0, c1) of each window
+        const i64 hc0 = (hA + 1) & ~(i64)1, hc1 = (hB + 1) & ~(i64)1;
+        const i64 lc0 = (l0 + 1) & ~(i64)1, lc1 = (l1 + 1) & ~(i64)1;
+        const u32 hbytes = hc1 > hc0 ? (u32)((hc1 - hc0) * 8) : 0u;
+        const u32 lbytes = lc1 > lc0 ? (u32)((lc1 - lc0) * 8) : 0u;
+        if (threadIdx.x == 0) {
+            mbar_init(&bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            // one arrival (with the byte count of both copies) completes the phase
+            mbar_expect_tx(&bar, hbytes + lbytes);
+            if (hbytes) bulk_g2s(stage + (hc0 - hA2), A.hpre + hc0, hbytes, &bar);
+            if (lbytes) bulk_g2s(stage + lbase + (lc0 - l02), A.lpre + lc0, lbytes, &bar);
+        }
+        // the odd ends (a window without a bulk part has at most two values)
+        if (threadIdx.x == 1 && (hA < hc0 || !hbytes)) stage[hA - hA2] = A.hpre[hA];
+        if (threadIdx.x == 2 && (hB >= hc1 || !hbytes)) stage[hB - hA2] = A.hpre[hB];
+        if (threadIdx.x == 3 && (l0 < lc0 || !lbytes)) stage[lbase + l0 - l02] = A.lpre[l0];
+        if (threadIdx.x == 4 && (l1 >= lc1 || !lbytes)) stage[lbase + l1 - l02] = A.lpre[l1];
+        __syncthreads();  // barrier initialised before anyone waits on it
+        mbar_wait(&bar, 0);
+    } else if (staged) {  // prefix views not 16-byte aligned: plain loads
+        for (i64 k = hA + threadIdx.x; k <= hB; k += blockDim.x) stage[k - hA2] = A.hpre[k];
+        for (i64 k = l0 + threadIdx.x; k <= l1; k += blockDim.x) stage[lbase + k - l02] = A.lpre[k];
     }
     __syncthreads();
     const u64 i = i0 + threadIdx.x;
@@ -366,8 +395,8 @@ __global__ void __launch_bounds__(PLAN_RUN) k_plan_batched(PlanArgs A, const T *
     i64 best = lo, a = lo, b = hi;
     while (a <= b) {
         i64 mid = (a + b) >> 1;
-        double L = staged ? stage[hlen + (ni - mid - l0)] : A.lpre[ni - mid];
-        double H = staged ? stage[mid - hA] : A.hpre[mid];
+        double L = staged ? stage[lbase + (ni - mid - l02)] : A.lpre[ni - mid];
+        double H = staged ? stage[mid - hA2] : A.hpre[mid];
         if (L + H <= cap) {
             best = mid;
             a = mid + 1;

@@ -29,6 +29,7 @@ for n, kind in ((1, 0), (7, 0), (2049, 1), (70_001, 0), (70_001, 2), (60_000, 3)
         assert t.count_unwritten() == 0
         p = ak.partition_items(ws)
         plan = ak.compute_split_plan(p, min(7, n))
+        ak.compute_split_plan(p, max(1, n // 16))  # many runs: TMA-staged windows
         ak.pack_section(p, plan, 1, ak.AliasTable.blank(n, ws.total, ws.dtype))
         tp = ak.psa_plus_construct(ws, block_size=64, threshold=4)
         assert tp.count_unwritten() == 0
