@@ -81,7 +81,7 @@ struct BuildWs {
     double *mD, *mE;        // [nt*8] chunk bounds (monotone inclusive scans)
     unsigned char *mfh;     // [nt*8] first heavy offset in chunk, NOFH if none
     unsigned short *mcl;    // [nt*8] lights in chunk
-    u32 *T1, *S1;           // [nt+1]
+    u32 *T1;                // [nt+1]
     u64 *nextH;             // [nt]
 };
 
@@ -102,7 +102,7 @@ template <typename F> inline void layout(u64 n, F &&take)
     size_t sizes[19] = {256,          nst * 4,      nst * 16,       nst * 16,       nst * 8,
                         nst * 16,     nst * 16,     nst * 8,        (nt + 1) * 16,  (nt + 1) * 16,
                         (nt + 1) * 8, nt * 8,       nt * NW * 8,    nt * NW * 8,    nt * NW,
-                        (nt + 1) * 4, (nt + 1) * 4, nt * 8,         nt * NW * 2};
+                        (nt + 1) * 4, 0,            nt * 8,         nt * NW * 2};  // [16]: unused
     for (int i = 0; i < 19; ++i) take(i, sizes[i]);
 }
 
@@ -135,7 +135,6 @@ inline BuildWs carve(void *ws, u64 n)
     W.mE = (double *)p[13];
     W.mfh = (unsigned char *)p[14];
     W.T1 = (u32 *)p[15];
-    W.S1 = (u32 *)p[16];
     W.nextH = (u64 *)p[17];
     W.mcl = (unsigned short *)p[18];
     return W;
@@ -568,34 +567,59 @@ __global__ void __launch_bounds__(SC_WARPS * 32) k_build_scan(const T *__restric
 // ---------------------------------------------------------------------------
 // 2. coarse merge of the tile boundaries
 // ---------------------------------------------------------------------------
-__global__ void k_build_coarse(BuildWs W, u64 n)
+// T1[u] = max{t : DHb[t] <= DLb[u]} for every section boundary u, as the
+// paper's generalised parallel search: T1 is non-decreasing in u, so a CTA
+// of 256 consecutive boundaries finds its first and last answer by two
+// global binary searches, stages the tile-base window DHb[T1(first) ..
+// T1(last)] in shared memory with one 1-D bulk async copy (TMA + mbarrier),
+// and each thread searches its boundary there.  Windows wider than CW
+// (rare: skewed inputs) search global memory instead.
+constexpr int CW = 2048;  // staged tile bases (double-double): 32 KB
+__global__ void __launch_bounds__(256) k_build_coarse(BuildWs W, u64 n)
 {
+    __shared__ __align__(16) dd win[CW];
+    __shared__ __align__(8) u64 bar;
+    __shared__ u64 ends[2];
     const u64 nt = W.nt;
-    u64 u = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (u > nt) return;
-    {  // T1[u] = max{t in [0, nt] : DHb[t] <= DLb[u]}
+    const u64 u0 = (u64)blockIdx.x * 256;
+    const u64 u1 = u0 + 255 < nt ? u0 + 255 : nt;
+    auto t1_global = [&](u64 u) {
         const dd x = W.DLb[u];
         u64 lo = 0, hi = nt;
         while (lo < hi) {
-            u64 mid = (lo + hi + 1) >> 1;
+            const u64 mid = (lo + hi + 1) >> 1;
             if (dd_le(W.DHb[mid], x)) lo = mid;
             else hi = mid - 1;
         }
-        W.T1[u] = (u32)lo;
-    }
-    {  // S1[u] = max{s in [0, nt] : DLb[s] < DHb[u]}, 0 if none
-        const dd y = W.DHb[u];
-        if (!dd_lt(W.DLb[0], y)) {
-            W.S1[u] = 0;
-        } else {
-            u64 lo = 0, hi = nt;
-            while (lo < hi) {
-                u64 mid = (lo + hi + 1) >> 1;
-                if (dd_lt(W.DLb[mid], y)) lo = mid;
-                else hi = mid - 1;
-            }
-            W.S1[u] = (u32)lo;
+        return lo;
+    };
+    if (threadIdx.x == 0) ends[0] = t1_global(u0);
+    if (threadIdx.x == 32) ends[1] = t1_global(u1);
+    __syncthreads();
+    const u64 ta = ends[0], tb = ends[1];
+    const u64 wl = tb - ta + 1;
+    const bool staged = wl <= (u64)CW;
+    if (staged) {
+        if (threadIdx.x == 0) {
+            mbar_init(&bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            mbar_expect_tx(&bar, (u32)(wl * sizeof(dd)));
+            bulk_g2s(win, W.DHb + ta, (u32)(wl * sizeof(dd)), &bar);
         }
+        __syncthreads();
+        mbar_wait(&bar, 0);
+    }
+    const u64 u = u0 + threadIdx.x;
+    if (u > u1) return;
+    {
+        const dd x = W.DLb[u];
+        u64 lo = ta, hi = tb;
+        while (lo < hi) {
+            const u64 mid = (lo + hi + 1) >> 1;
+            if (dd_le(staged ? win[mid - ta] : W.DHb[mid], x)) lo = mid;
+            else hi = mid - 1;
+        }
+        W.T1[u] = (u32)lo;
     }
     if (u < nt) {  // nextH[u]: first heavy item in tiles > u
         auto jH = [&](u64 t) -> u64 {
