@@ -273,3 +273,43 @@ def test_n_1e9_against_reference_psa(dtype, acceptance):
     acceptance(f"PASS  N=1e9 uniform {str(dtype)[6:]}: every row written; vs PSA(s=N/1024) {flips} "
                f"alias flips + {moved} moved heavy closes, all near-ties (worst margin {worst:.1e} avg "
                f"< tau {tau(n):.1e}); other heavy tw within {pgap:.1e} avg; {rep}")
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_extreme_inputs(rng, dtype):
+    """Inputs at the edges of the number formats and of the pairing logic:
+    f32 subnormals among normal weights, a 1e-200..1e200 dynamic range (f64),
+    one weight holding almost all the mass (a heavy spanning every section),
+    many items exactly at the average (zero-deficit lights: key ties), tiny
+    n.  Alias indices equal the drift-free sequential order except at
+    certified exact ties; every row is written; per-item mass holds."""
+    cases = []
+    if dtype == torch.float32:
+        sub = rng.random(50_000).astype(np.float32) * np.float32(1e-39)   # subnormal f32
+        sub[sub == 0] = np.float32(1e-45)
+        cases.append(np.concatenate([sub, rng.random(50_000).astype(np.float32) + np.float32(0.5)]))
+    else:
+        cases.append(10.0 ** rng.uniform(-200, 200, 100_000))
+    big = rng.random(1_000_000) + 1e-3
+    big[123_457] = 1e12                                                # 99.9998% of the mass
+    cases.append(big)
+    eq = np.full(200_001, 2.0)                                          # exactly-average lights
+    eq[::7] = 1.0
+    eq[3::7] = 3.0                                                      # balanced: avg stays 2
+    cases.append(eq)
+    for n in (1, 2, 3):
+        cases.append(rng.random(n) + 0.1)
+    for w in cases:
+        w = np.asarray(w, dtype=np.float32 if dtype == torch.float32 else np.float64)
+        rng.shuffle(w)
+        ws = ak.make_weight_set(torch.from_numpy(np.ascontiguousarray(w)).to(DEV))
+        t = ak.psa_construct(ws)
+        assert t.count_unwritten() == 0
+        w64 = ws.weights.double().cpu().numpy()
+        q = O.vose_construct_quad(w64, ws.total)
+        diff = np.flatnonzero(t.to_numpy()[1] != q.alias)
+        if diff.size:
+            m = O.decision_margins(w64, ws.total, diff + 1)
+            assert float(np.max(m)) < 1e-9, (w.size, diff.size, float(np.max(m)))
+        rep = ak.validate_table(t, ws, tol=1e-9 if dtype == torch.float64 else 1e-4)
+        assert rep.ok, (w.size, rep)
