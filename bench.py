@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--rng", default="philox4x32", choices=["philox4x32", "reference"])
     ap.add_argument("--dtype", default="float32", choices=["float32", "float64"])
     ap.add_argument("--e2e-samples", type=float, default=2e9)
-    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--cpu-n", type=float, default=1e8)
     ap.add_argument("--cpu-samples", type=float, default=2e8)
     ap.add_argument("--ref-samples", type=float, default=1e8,

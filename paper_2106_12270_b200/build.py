@@ -24,7 +24,7 @@ OBJ = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "libaliaskit_b200.so")
 
 CU_SOURCES = ["ak_sample.cu", "ak_weights.cu", "ak_partition.cu", "ak_build.cu", "ak_verify.cu",
-              "ak_prepack.cu"]
+              "ak_prepack.cu", "ak_util.cu"]
 CPP_SOURCES = ["ak_host.cpp"]
 HEADERS = ["ak_common.cuh"]
 

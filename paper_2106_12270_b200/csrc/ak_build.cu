@@ -1101,8 +1101,11 @@ int run_build(const void *wv, u64 n, double avg, void *rows, void *ws, cudaStrea
         O.hchunk = O.hrank + (W.nt + 2);
         O.hitem = O.hchunk + (W.nt + 2);
     }
-    AK_CUDA_TRY(cudaMemsetAsync(W.counter, 0, 256, st));
-    AK_CUDA_TRY(cudaMemsetAsync(W.status, 0, W.nst * 4, st));
+    {
+        int rc = ak_fill_small(W.counter, 0, 256, st);
+        if (rc == AK_OK) rc = ak_fill_small(W.status, 0, W.nst * 4, st);
+        if (rc != AK_OK) return rc;
+    }
     AK_SMEM_ATTR(k_build_scan<T>, (int)ScanBuf<T>::BYTES);
     k_build_scan<T><<<(unsigned)W.nst, SC_WARPS * 32, ScanBuf<T>::BYTES, st>>>(w, n, avg, W);
     AK_LAUNCH_CHECK("k_build_scan");
@@ -1158,8 +1161,10 @@ int ak_build_stats(const void *ws, uint64_t n, uint64_t *nl, uint64_t *nh, uint6
     BuildWs W = carve(const_cast<void *>(ws), n);
     u64 k = 0;
     cudaStream_t st = ak_stream(stream);
-    AK_CUDA_TRY(cudaMemcpyAsync(&k, W.kL + W.nt, sizeof(u64), cudaMemcpyDeviceToHost, st));
-    AK_CUDA_TRY(cudaStreamSynchronize(st));
+    {
+        const int rc = ak_readback(st, &k, W.kL + W.nt, sizeof(u64));
+        if (rc != AK_OK) return rc;
+    }
     *nl = k;
     *nh = n - k;
     *tiles = W.nt;

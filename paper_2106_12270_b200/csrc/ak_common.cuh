@@ -41,6 +41,14 @@ static inline cudaStream_t ak_stream(void *s) { return (cudaStream_t)s; }
 
 int ak_num_sms();
 void *ak_stream_scratch(cudaStream_t st);  // 256 B per (host thread, device, stream)
+void *ak_mailbox(cudaStream_t st);         // 256 B mapped pinned host memory, same keying
+// Small device results (up to 3 pieces, <= 256 bytes in all) to host memory
+// through the mailbox: one-block kernel, then a synchronisation of st only.
+int ak_readback(cudaStream_t st, void *dst0, const void *src0, size_t n0, void *dst1 = nullptr,
+                const void *src1 = nullptr, size_t n1 = 0, void *dst2 = nullptr,
+                const void *src2 = nullptr, size_t n2 = 0);
+// A small device fill by a kernel (no copy engine): bytes of value `byte`.
+int ak_fill_small(void *p, int byte, size_t bytes, cudaStream_t st);
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
 // the launch paths call this instead of the driver on every call
 cudaError_t ak_smem_attr_once(const void *kernel, int bytes);

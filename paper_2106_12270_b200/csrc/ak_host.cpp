@@ -73,6 +73,35 @@ void *ak_stream_scratch(cudaStream_t st)
     return p;
 }
 
+// 256 bytes of mapped pinned host memory per (host thread, device, stream):
+// the mailbox a one-block kernel stores an entry point's small results into
+// (ak_readback).  Kernel stores over PCIe need no copy engine, so a result
+// readback does not queue behind bulk host<->device copies other streams
+// have in flight on the copy engines (a cudaMemcpyAsync of 8 bytes does).
+namespace {
+struct ThreadMailbox {
+    std::map<std::pair<int, cudaStream_t>, void *> bufs;
+    ~ThreadMailbox()
+    {
+        for (auto &kv : bufs) cudaFreeHost(kv.second);
+    }
+};
+}  // namespace
+
+void *ak_mailbox(cudaStream_t st)
+{
+    static thread_local ThreadMailbox tm;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    auto key = std::make_pair(dev, st);
+    auto it = tm.bufs.find(key);
+    if (it != tm.bufs.end()) return it->second;
+    void *p = nullptr;
+    if (cudaHostAlloc(&p, 256, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) return nullptr;
+    tm.bufs[key] = p;
+    return p;
+}
+
 cudaError_t ak_smem_attr_once(const void *kernel, int bytes)
 {
     static std::mutex mu;

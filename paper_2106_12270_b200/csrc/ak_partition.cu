@@ -641,8 +641,10 @@ int run_partition(const void *wv, u64 n, double avg, i64 *l_idx, void *l_w, i64 
                                                               h_idx, (T *)h_w, lpre, hpre, tot);
     AK_LAUNCH_CHECK("k_part_scatter");
     PartAgg t;
-    AK_CUDA_TRY(cudaMemcpyAsync(&t, tot, sizeof(t), cudaMemcpyDeviceToHost, st));
-    AK_CUDA_TRY(cudaStreamSynchronize(st));
+    {
+        const int rc = ak_readback(st, &t, tot, sizeof(t));
+        if (rc != AK_OK) return rc;
+    }
     *nl_out = t.nl;
     *nh_out = n - t.nl;
     return AK_OK;
@@ -739,13 +741,18 @@ int ak_partial_pary_search(const double *hay, uint64_t n, const double *q, uint6
     int *flag = (int *)ak_stream_scratch(st);
     if (!flag) return AK_ERR_CUDA;
     i64 *ab = (i64 *)((char *)flag + 16);
-    AK_CUDA_TRY(cudaMemsetAsync(flag, 0, 2 * sizeof(int), st));
+    {
+        const int rc0 = ak_fill_small(flag, 0, 2 * sizeof(int), st);
+        if (rc0 != AK_OK) return rc0;
+    }
     const unsigned g = (unsigned)ak_num_sms() * 8;
     if (n > 1) k_check_sorted<<<g, 256, 0, st>>>(hay, n, flag);
     if (m > 1) k_check_sorted<<<g, 256, 0, st>>>(q, m, flag + 1);
     int f[2] = {0, 0};
-    AK_CUDA_TRY(cudaMemcpyAsync(f, flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-    AK_CUDA_TRY(cudaStreamSynchronize(st));
+    {
+        const int rc0 = ak_readback(st, f, flag, 2 * sizeof(int));
+        if (rc0 != AK_OK) return rc0;
+    }
     AK_LAUNCH_CHECK("k_check_sorted");
     int rc = AK_OK;
     if (f[0] || f[1]) rc = AK_ERR_UNSORTED_INPUT;

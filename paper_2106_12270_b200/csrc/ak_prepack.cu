@@ -578,7 +578,10 @@ int ak_greedy_prepack(const void *w, int dtype, uint64_t n, double avg, uint32_t
     i64 *tot = (i64 *)(p + 64);
     const size_t rb = dtype == AK_F32 ? 8 : 16;
     AK_CUDA_TRY(cudaMemsetAsync(rows, 0, n * rb, st));
-    AK_CUDA_TRY(cudaMemsetAsync(nw, 0, 8, st));
+    {
+        const int rc0 = ak_fill_small(nw, 0, 8, st);
+        if (rc0 != AK_OK) return rc0;
+    }
     if (dtype == AK_F32) {
         AK_SMEM_ATTR(k_prepack_block<float>, (int)smem);
         k_prepack_block<float><<<(unsigned)nb, PP_TB, smem, st>>>((const float *)w, n, avg, block_size,
@@ -604,9 +607,10 @@ int ak_greedy_prepack(const void *w, int dtype, uint64_t n, double avg, uint32_t
     AK_LAUNCH_CHECK("k_prepack_emit");
     i64 nres = 0;
     unsigned long long nwr = 0;
-    AK_CUDA_TRY(cudaMemcpyAsync(&nres, tot, 8, cudaMemcpyDeviceToHost, st));
-    AK_CUDA_TRY(cudaMemcpyAsync(&nwr, nw, 8, cudaMemcpyDeviceToHost, st));
-    AK_CUDA_TRY(cudaStreamSynchronize(st));
+    {
+        const int rc = ak_readback(st, &nres, tot, 8, &nwr, nw, 8);
+        if (rc != AK_OK) return rc;
+    }
     *nres_out = (u64)nres;
     *nwritten_out = (u64)nwr;
     return AK_OK;

@@ -198,8 +198,11 @@ int run_validate(const void *rows, u64 n, u64 ilo, u64 ihi, const void *w, doubl
     unsigned long long *misc = (unsigned long long *)(lo + m);  // [0] worst, [1] first
     int *bad = (int *)(misc + 2);
     AK_CUDA_TRY(cudaMemsetAsync(hi, 0, 2 * m * sizeof(double), st));
-    AK_CUDA_TRY(cudaMemsetAsync(misc, 0, 2 * sizeof(unsigned long long) + 16, st));
-    AK_CUDA_TRY(cudaMemsetAsync(misc + 1, 0xff, sizeof(unsigned long long), st));
+    {
+        int rc0 = ak_fill_small(misc, 0, 2 * sizeof(unsigned long long) + 16, st);
+        if (rc0 == AK_OK) rc0 = ak_fill_small(misc + 1, 0xff, sizeof(unsigned long long), st);
+        if (rc0 != AK_OK) return rc0;
+    }
     k_donate<RowT><<<grid_of(n), 256, 0, st>>>((const RowT *)rows, n, ilo, ihi, avg, row_tol, hi, lo, bad);
     if (m) {
         k_mass<RowT, W><<<grid_of(m), 256, 0, st>>>((const RowT *)rows, (const W *)w, ilo, ihi, hi, lo, misc);
@@ -209,9 +212,10 @@ int run_validate(const void *rows, u64 n, u64 ilo, u64 ihi, const void *w, doubl
     AK_LAUNCH_CHECK("k_validate");
     unsigned long long hm[2];
     int b = 0;
-    AK_CUDA_TRY(cudaMemcpyAsync(hm, misc, sizeof(hm), cudaMemcpyDeviceToHost, st));
-    AK_CUDA_TRY(cudaMemcpyAsync(&b, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-    AK_CUDA_TRY(cudaStreamSynchronize(st));
+    {
+        const int rc = ak_readback(st, hm, misc, sizeof(hm), &b, bad, sizeof(int));
+        if (rc != AK_OK) return rc;
+    }
     *rows_ok = !b;
     *worst_rel = m ? __builtin_bit_cast(double, hm[0]) : 0.0;
     *worst_item = m ? (int64_t)hm[1] + 1 : 0;
@@ -263,7 +267,10 @@ int ak_chi2_partial(const int64_t *counts, const void *w, int w_dtype, uint64_t 
                     double total_w, double draws, double *out4, void *stream)
 {
     cudaStream_t st = ak_stream(stream);
-    AK_CUDA_TRY(cudaMemsetAsync(out4, 0, 4 * sizeof(double), st));
+    {
+        const int rc0 = ak_fill_small(out4, 0, 4 * sizeof(double), st);
+        if (rc0 != AK_OK) return rc0;
+    }
     if (m == 0) return AK_OK;
     if (w_dtype == AK_F32)
         k_chi2_partial<float><<<grid_of(m), 256, 0, st>>>(counts, (const float *)w, m, total_w, draws, out4);
@@ -282,12 +289,17 @@ int ak_frequency_counts(const int64_t *samples, uint64_t m, uint64_t n, int64_t 
     if (n < 1) return AK_ERR_VALUE;
     int *oor = (int *)ak_stream_scratch(st);
     if (!oor) return AK_ERR_CUDA;
-    AK_CUDA_TRY(cudaMemsetAsync(oor, 0, 16, st));
+    {
+        const int rc = ak_fill_small(oor, 0, 16, st);
+        if (rc != AK_OK) return rc;
+    }
     AK_CUDA_TRY(cudaMemsetAsync(counts, 0, n * sizeof(int64_t), st));
     if (m) k_freq<<<grid_of(m), 256, 0, st>>>(samples, m, n, (unsigned long long *)counts, oor);
     int f = 0;
-    AK_CUDA_TRY(cudaMemcpyAsync(&f, oor, sizeof(int), cudaMemcpyDeviceToHost, st));
-    AK_CUDA_TRY(cudaStreamSynchronize(st));
+    {
+        const int rc = ak_readback(st, &f, oor, sizeof(int));
+        if (rc != AK_OK) return rc;
+    }
     AK_LAUNCH_CHECK("k_freq");
     return f ? AK_ERR_INDEX_OUT_OF_RANGE : AK_OK;
 }
@@ -335,14 +347,19 @@ int ak_count_unwritten(const void *rows, int dtype, uint64_t n, uint64_t *unwrit
     if (dtype != AK_F32 && dtype != AK_F64) return AK_ERR_VALUE;
     unsigned long long *c = (unsigned long long *)ak_stream_scratch(st);
     if (!c) return AK_ERR_CUDA;
-    AK_CUDA_TRY(cudaMemsetAsync(c, 0, 16, st));
+    {
+        const int rc = ak_fill_small(c, 0, 16, st);
+        if (rc != AK_OK) return rc;
+    }
     if (n) {
         if (dtype == AK_F32) k_unwritten<RowF32><<<grid_of(n), 256, 0, st>>>((const RowF32 *)rows, n, c);
         else k_unwritten<RowF64><<<grid_of(n), 256, 0, st>>>((const RowF64 *)rows, n, c);
     }
     unsigned long long h = 0;
-    AK_CUDA_TRY(cudaMemcpyAsync(&h, c, sizeof(h), cudaMemcpyDeviceToHost, st));
-    AK_CUDA_TRY(cudaStreamSynchronize(st));
+    {
+        const int rc = ak_readback(st, &h, c, sizeof(h));
+        if (rc != AK_OK) return rc;
+    }
     AK_LAUNCH_CHECK("k_unwritten");
     *unwritten = h;
     return AK_OK;

@@ -326,7 +326,10 @@ int ak_weights_validate_total(const void *w, int dtype, uint64_t n, double *tota
     unsigned long long *bad = (unsigned long long *)base;
     double *part = (double *)(base + 256);
     double *part2 = part + ((size_t)1 << D);
-    AK_CUDA_TRY(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
+    {
+        const int rc = ak_fill_small(bad, 0xff, sizeof(unsigned long long), st);
+        if (rc != AK_OK) return rc;
+    }
     const u64 nthreads = 1ull << D;
     const unsigned g = (unsigned)((nthreads + PW_WARPS - 1) / PW_WARPS);
     const int tb = PW_WARPS * 32;
@@ -351,9 +354,10 @@ int ak_weights_validate_total(const void *w, int dtype, uint64_t n, double *tota
     }
     double tot = 0.0;
     unsigned long long b = 0;
-    AK_CUDA_TRY(cudaMemcpyAsync(&tot, src, sizeof(double), cudaMemcpyDeviceToHost, st));
-    AK_CUDA_TRY(cudaMemcpyAsync(&b, bad, sizeof(b), cudaMemcpyDeviceToHost, st));
-    AK_CUDA_TRY(cudaStreamSynchronize(st));
+    {
+        const int rc = ak_readback(st, &tot, src, sizeof(double), &b, bad, sizeof(b));
+        if (rc != AK_OK) return rc;
+    }
     if (b != ~0ull) {
         *bad_index = (int64_t)b;
         return AK_ERR_INVALID_WEIGHT;
