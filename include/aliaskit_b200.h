@@ -187,6 +187,18 @@ int ak_greedy_prepack(const void *w, int dtype, uint64_t n, double avg, uint32_t
  * mapped back to item ids (pack.py:297-299). */
 int ak_residual_scatter(const void *res_rows, const int64_t *res_idx, uint64_t nres, double avg,
                         int dtype, void *rows, void *stream);
+/* ak_greedy_prepack with the row clearing optional (clear_rows = 0: rows the
+ * prepack does not pair keep their contents; psa_plus fills them all). */
+int ak_greedy_prepack_ex(const void *w, int dtype, uint64_t n, double avg, uint32_t block_size,
+                         uint32_t threshold, int clear_rows, void *rows, int64_t *res_idx,
+                         double *res_w, uint64_t *nres_out, uint64_t *nwritten_out, void *ws,
+                         size_t ws_bytes, void *stream);
+/* ak_residual_scatter that also returns how many rows it wrote with a
+ * nonzero alias (a written bucket): with the prepack's own count, PSA+'s
+ * "every bucket written" check (pack.py:303-304) without a pass over the
+ * table. */
+int ak_residual_scatter_count(const void *res_rows, const int64_t *res_idx, uint64_t nres,
+                              double avg, int dtype, void *rows, uint64_t *written, void *stream);
 
 /* ---- sampling (sample.py) ----------------------------------------------- */
 

@@ -52,6 +52,9 @@ _SIGS = {
     "ak_greedy_prepack": (ci, [vp, ci, u64, dbl, C.c_uint32, C.c_uint32, vp, vp, vp, vp, vp, vp,
                                sz, vp]),
     "ak_residual_scatter": (ci, [vp, vp, u64, dbl, ci, vp, vp]),
+    "ak_residual_scatter_count": (ci, [vp, vp, u64, dbl, ci, vp, vp, vp]),
+    "ak_greedy_prepack_ex": (ci, [vp, ci, u64, dbl, C.c_uint32, C.c_uint32, ci, vp, vp, vp, vp, vp, vp,
+                                  sz, vp]),
     "ak_sample_naive": (ci, [vp, ci, u64, dbl, u64, u64, u64, u64, u64, u64, vp, ci, vp]),
     "ak_sample_naive_out": (ci, [vp, ci, u64, dbl, u64, u64, u64, u64, u64, u64, vp, ci, ci, vp]),
     "ak_sample_from_uniforms": (ci, [vp, ci, u64, dbl, u64, u64, vp, u64, vp, vp]),

@@ -522,20 +522,30 @@ __global__ void k_excl_scan_i64(const i64 *cnt, u64 nb, i64 *off, i64 *total)
     if (threadIdx.x == 0) *total = carry;
 }
 
-// residual table (f64 rows over residual positions) -> final rows
+// residual table (f64 rows over residual positions) -> final rows; with
+// `written` non-null, also counts the rows it writes with a nonzero alias
+// (a written bucket) — the residual half of PSA+'s every-bucket-written check
 template <typename RowOut>
 __global__ void k_residual_remap(const RowF64 *__restrict__ rt, const i64 *__restrict__ res_idx,
-                                 u64 nres, double avg, RowOut *__restrict__ rows)
+                                 u64 nres, double avg, RowOut *__restrict__ rows,
+                                 unsigned long long *written)
 {
     typedef decltype(RowOut::tw) TwT;
     typedef decltype(RowOut::alias) AliasT;
     const u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= nres) return;
-    const RowF64 x = rt[r];
-    RowOut o;
-    o.tw = tw_store<TwT>(x.tw, avg);
-    o.alias = (AliasT)res_idx[x.alias - 1];
-    rows[res_idx[r] - 1] = o;
+    bool ok = false;
+    if (r < nres) {
+        const RowF64 x = rt[r];
+        RowOut o;
+        o.tw = tw_store<TwT>(x.tw, avg);
+        o.alias = x.alias ? (AliasT)res_idx[x.alias - 1] : (AliasT)0;
+        ok = o.alias != 0;
+        rows[res_idx[r] - 1] = o;
+    }
+    if (written) {
+        const unsigned b = __ballot_sync(0xffffffffu, ok);
+        if ((threadIdx.x & 31) == 0 && b) atomicAdd(written, (unsigned long long)__popc(b));
+    }
 }
 
 size_t pp_smem_bytes(u32 bs, size_t wb) { return (((size_t)bs * wb + 15) & ~(size_t)15) + (size_t)(pk(bs + 2) + 1) * 8 + (size_t)bs * 2 + 16; }
@@ -560,6 +570,15 @@ int ak_greedy_prepack(const void *w, int dtype, uint64_t n, double avg, uint32_t
                       uint64_t *nres_out, uint64_t *nwritten_out, void *ws, size_t ws_bytes,
                       void *stream)
 {
+    return ak_greedy_prepack_ex(w, dtype, n, avg, block_size, threshold, 1, rows, res_idx, res_w,
+                                nres_out, nwritten_out, ws, ws_bytes, stream);
+}
+
+int ak_greedy_prepack_ex(const void *w, int dtype, uint64_t n, double avg, uint32_t block_size,
+                         uint32_t threshold, int clear_rows, void *rows, int64_t *res_idx,
+                         double *res_w, uint64_t *nres_out, uint64_t *nwritten_out, void *ws,
+                         size_t ws_bytes, void *stream)
+{
     if (n == 0) return AK_ERR_EMPTY_INPUT;
     if (block_size < 2 || threshold < 1) return AK_ERR_VALUE;
     const size_t smem = pp_smem_bytes(block_size, dtype == AK_F32 ? 4 : 8);
@@ -577,7 +596,7 @@ int ak_greedy_prepack(const void *w, int dtype, uint64_t n, double avg, uint32_t
     unsigned long long *nw = (unsigned long long *)p;
     i64 *tot = (i64 *)(p + 64);
     const size_t rb = dtype == AK_F32 ? 8 : 16;
-    AK_CUDA_TRY(cudaMemsetAsync(rows, 0, n * rb, st));
+    if (clear_rows) AK_CUDA_TRY(cudaMemsetAsync(rows, 0, n * rb, st));
     {
         const int rc0 = ak_fill_small(nw, 0, 8, st);
         if (rc0 != AK_OK) return rc0;
@@ -616,22 +635,43 @@ int ak_greedy_prepack(const void *w, int dtype, uint64_t n, double avg, uint32_t
     return AK_OK;
 }
 
-int ak_residual_scatter(const void *res_rows, const int64_t *res_idx, uint64_t nres, double avg,
-                        int dtype, void *rows, void *stream)
+static int residual_scatter(const void *res_rows, const int64_t *res_idx, uint64_t nres, double avg,
+                            int dtype, void *rows, unsigned long long *written, cudaStream_t st)
 {
-    if (nres == 0) return AK_OK;
-    cudaStream_t st = ak_stream(stream);
     const unsigned g = (unsigned)((nres + 255) / 256);
     if (dtype == AK_F32)
         k_residual_remap<RowF32><<<g, 256, 0, st>>>((const RowF64 *)res_rows, res_idx, nres, avg,
-                                                     (RowF32 *)rows);
+                                                     (RowF32 *)rows, written);
     else if (dtype == AK_F64)
         k_residual_remap<RowF64><<<g, 256, 0, st>>>((const RowF64 *)res_rows, res_idx, nres, avg,
-                                                     (RowF64 *)rows);
+                                                     (RowF64 *)rows, written);
     else
         return AK_ERR_VALUE;
     AK_LAUNCH_CHECK("k_residual_remap");
     return AK_OK;
+}
+
+int ak_residual_scatter(const void *res_rows, const int64_t *res_idx, uint64_t nres, double avg,
+                        int dtype, void *rows, void *stream)
+{
+    if (nres == 0) return AK_OK;
+    return residual_scatter(res_rows, res_idx, nres, avg, dtype, rows, nullptr, ak_stream(stream));
+}
+
+int ak_residual_scatter_count(const void *res_rows, const int64_t *res_idx, uint64_t nres,
+                              double avg, int dtype, void *rows, uint64_t *written, void *stream)
+{
+    *written = 0;
+    if (nres == 0) return AK_OK;
+    cudaStream_t st = ak_stream(stream);
+    unsigned long long *c = (unsigned long long *)ak_stream_scratch(st);
+    if (!c) return AK_ERR_CUDA;
+    int rc = ak_fill_small(c, 0, 8, st);
+    if (rc == AK_OK) rc = residual_scatter(res_rows, res_idx, nres, avg, dtype, rows, c, st);
+    unsigned long long h = 0;
+    if (rc == AK_OK) rc = ak_readback(st, &h, c, sizeof(h));
+    *written = h;
+    return rc;
 }
 
 }  // extern "C"

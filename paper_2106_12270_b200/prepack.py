@@ -24,7 +24,7 @@ from .partition import LightHeavyPartition, PrepackResult
 MAX_BLOCK = 11000  # 20 bytes of shared memory per item of a block (ak_prepack.cu)
 
 
-def _prepack(w: WeightSet, block_size: int, threshold: int):
+def _prepack(w: WeightSet, block_size: int, threshold: int, clear_rows: bool = True):
     if block_size < 2:
         raise ValueError("block_size must be at least 2")
     if threshold < 1:
@@ -42,11 +42,11 @@ def _prepack(w: WeightSet, block_size: int, threshold: int):
     nres = C.c_uint64(0)
     nw = C.c_uint64(0)
     with torch.cuda.device(dev):
-        _lib.check(L.ak_greedy_prepack(_lib.ptr(w.weights), _lib.dtype_code(w.weights.dtype), n,
-                                       w.average, block_size, threshold, _lib.ptr(t.rows),
-                                       _lib.ptr(res_idx), _lib.ptr(res_w), C.byref(nres),
-                                       C.byref(nw), _lib.ptr(ws), ws.numel(),
-                                       _lib.stream_ptr(dev)), "greedy_prepack")
+        _lib.check(L.ak_greedy_prepack_ex(_lib.ptr(w.weights), _lib.dtype_code(w.weights.dtype), n,
+                                          w.average, block_size, threshold, int(clear_rows),
+                                          _lib.ptr(t.rows), _lib.ptr(res_idx), _lib.ptr(res_w),
+                                          C.byref(nres), C.byref(nw), _lib.ptr(ws), ws.numel(),
+                                          _lib.stream_ptr(dev)), "greedy_prepack")
     k = int(nres.value)
     return t, res_idx[:k], res_w[:k], int(nw.value)
 
@@ -74,8 +74,14 @@ def psa_plus_construct(w: WeightSet, s: int = 64, block_size: int = 4096,
                        threshold: int = 8) -> AliasTable:
     """Split construction preceded by the block-local pairing pass
     (pack.py:280-305); the residual goes through the fused PSA pipeline with
-    the global average (the section count ``s`` does not change the table)."""
-    t, res_idx, res_w, _ = _prepack(w, block_size, threshold)
+    the global average (the section count ``s`` does not change the table).
+
+    The reference's closing check, every bucket written (pack.py:303-304),
+    is made from counts instead of a pass over the table: the prepack counts
+    the rows it pairs, the residual scatter the rows it writes with a nonzero
+    alias, and the two sets are disjoint by construction — so the table is
+    not cleared first and not re-read afterwards."""
+    t, res_idx, res_w, nwritten = _prepack(w, block_size, threshold, clear_rows=False)
     k = res_idx.numel()
     dev = w.weights.device
     L = _lib.lib()
@@ -87,9 +93,12 @@ def psa_plus_construct(w: WeightSet, s: int = 64, block_size: int = 4096,
             _lib.check(L.ak_build_psa_avg(_lib.ptr(res_w), _lib.F64, k, w.average, _lib.ptr(rt),
                                           _lib.ptr(ws), ws.numel(), _lib.stream_ptr(dev)),
                        "psa_plus residual build")
-            _lib.check(L.ak_residual_scatter(_lib.ptr(rt), _lib.ptr(res_idx), k, w.average,
-                                             t.dtype_code, _lib.ptr(t.rows), _lib.stream_ptr(dev)),
+            scattered = C.c_uint64(0)
+            _lib.check(L.ak_residual_scatter_count(_lib.ptr(rt), _lib.ptr(res_idx), k, w.average,
+                                                   t.dtype_code, _lib.ptr(t.rows),
+                                                   C.byref(scattered), _lib.stream_ptr(dev)),
                        "psa_plus residual scatter")
-    if t.count_unwritten() != 0:
+            nwritten += int(scattered.value)
+    if nwritten != w.n:
         raise PlanInconsistent("pack left buckets unwritten")
     return t
