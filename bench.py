@@ -596,7 +596,9 @@ def run_ours(a):
             "table_broadcast": bcast,
             "step_variant": ("rank 0 builds, NCCL broadcast of the table every step" if bcast_step
                              else "every rank rebuilds the table from its replicated weights"),
-            "gpu_launches": a.steps * (4 + len(passes)),
+            # per step: the build (2 scratch fills + scan, coarse split, split, pack)
+            # and one sectioned-sampling launch per pass
+            "gpu_launches": a.steps * (6 + len(passes)),
             "clocks": clocks,
             "wall_s_timed_region": wall,
         }
