@@ -542,9 +542,9 @@ __global__ void k_residual_remap(const RowF64 *__restrict__ rt, const i64 *__res
         ok = o.alias != 0;
         rows[res_idx[r] - 1] = o;
     }
-    if (written) {
-        const unsigned b = __ballot_sync(0xffffffffu, ok);
-        if ((threadIdx.x & 31) == 0 && b) atomicAdd(written, (unsigned long long)__popc(b));
+    if (written) {  // one atomic per block (every thread reaches the count)
+        const int c = __syncthreads_count(ok);
+        if (threadIdx.x == 0 && c) atomicAdd(written, (unsigned long long)c);
     }
 }
 
