@@ -47,3 +47,21 @@ def test_our_arm_contract():
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0 and d["scaling"] == "weak"
+
+
+@pytest.mark.gpu
+def test_reference_arm_weights_match_gpu_arm():
+    """bench.py --impl reference regenerates the GPU arm's weights on the host
+    (gen_uniform(N, RngStream(seed=1)) cast to float32, upcast to float64):
+    bit-identical to the device generator's."""
+    import numpy as np
+    import torch
+
+    sys.path.insert(0, ROOT)
+    import bench
+    import paper_2106_12270_b200 as ak
+
+    n = 1_000_003
+    host = bench.reference_weights(n)
+    dev = ak.gen_uniform(n, ak.RngStream(seed=1), dtype=torch.float32).weights.double().cpu().numpy()
+    assert np.array_equal(host, dev)
