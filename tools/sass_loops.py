@@ -10,7 +10,8 @@ import collections
 import re
 import subprocess
 
-LIB = "paper_2106_12270_b200/libaliaskit_b200.so"
+import os
+LIB = os.environ.get("SASS_LIB", "paper_2106_12270_b200/libaliaskit_b200.so")
 
 
 def main():
