@@ -19,8 +19,9 @@
 // Keys are block-local doubles (|key| <= block_size * avg), so decisions agree
 // with the reference's f64 chain except at ties inside its rounding noise.
 //
-//   k_prepack_block   classify, compact, keys, write handled rows, per-block
-//                     residual summary
+//   k_prepack_block   classify (thread = P consecutive items), CTA scan,
+//                     compacted keys, merge, handled rows, per-block residual
+//                     summary
 //   k_prepack_emit    residual items (index, weight) in global item order
 //   k_residual_remap  the residual table (built by the fused builder with the
 //                     global average) scattered into the final table
@@ -68,37 +69,11 @@ template <typename T> struct ClassCut {
     __device__ __forceinline__ int operator()(T v) const { return v < a ? 0 : (exact && v == a ? 2 : 1); }
 };
 
-// exclusive block scan of two counters (PP_TB threads)
-__device__ __forceinline__ void block_scan2(u32 a, u32 b, u32 &ea, u32 &eb, u32 &ta, u32 &tb)
-{
-    __shared__ u32 sa[PP_TB / 32], sb[PP_TB / 32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    u32 ia = a, ib = b;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const u32 x = __shfl_up_sync(0xffffffffu, ia, d), y = __shfl_up_sync(0xffffffffu, ib, d);
-        if (lane >= d) { ia += x; ib += y; }
-    }
-    if (lane == 31) { sa[wid] = ia; sb[wid] = ib; }
-    __syncthreads();
-    u32 oa = 0, ob = 0;
-    ta = tb = 0;
-    for (int k = 0; k < PP_TB / 32; ++k) {
-        if (k < wid) { oa += sa[k]; ob += sb[k]; }
-        ta += sa[k];
-        tb += sb[k];
-    }
-    ea = oa + ia - a;
-    eb = ob + ib - b;
-    __syncthreads();
-}
-
 // Dynamic shared memory of a block of bs items: the raw weights (staged
 // once), the class-compacted keys (logical index: lights [0, nl] with DL(nl)
-// at nl, heavies from nl + 1; stored at pk(x) = x + x/8 so that a lane's 8
-// consecutive keys are bank-conflict free) and block offsets (lights [0, nl),
-// heavies from nl).  Per-(row, warp) class counts and offsets are static.
-constexpr int PP_MAXR = (11000 + PP_TB - 1) / PP_TB;  // rows of PP_TB items per block
+// at nl, heavies from nl + 1; stored at pk(x) = x + x/8 to spread the
+// merge's key loads over the banks) and block offsets (lights [0, nl),
+// heavies from nl).
 __host__ __device__ __forceinline__ u32 pk(u32 x) { return x + (x >> 3); }
 template <typename T> struct PPSmem {
     T *sw;
@@ -114,89 +89,37 @@ template <typename T> __device__ __forceinline__ PPSmem<T> pp_smem(unsigned char
     return S;
 }
 
-// In-place monotone prefix over the logical keys [a0, a0 + cnt) (exclusive
-// or inclusive), in item order.  Chunks of 256 (lane l: 8 consecutive keys)
-// go to the warps round-robin: each lane forms its sequential local prefix,
-// a warp scan (Kogge-Stone, then a running max) of the lane totals gives the
-// lane offsets, and every value is clamped to its lane's upper bound, so the
-// chunk-local values are non-decreasing and end at the chunk total.  Chunk
-// offsets are then the sequential sums of the chunk totals.  Every step adds
-// a non-negative term to a non-decreasing value (or clamps), so the keys are
-// non-decreasing throughout (the merge needs sorted keys).  Returns the total.
-__device__ __forceinline__ double block_prefix(double *key, u32 a0, u32 cnt, bool exclusive)
-{
-    __shared__ double ctot[PP_MAXR + 1];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const u32 C = (cnt + 255) / 256;
-    for (u32 c = wid; c < C; c += PP_TB / 32) {
-        const u32 e0 = c * 256 + lane * 8;
-        double v[8], s = 0.0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const double x = e0 + q < cnt ? key[pk(a0 + e0 + q)] : 0.0;
-            if (exclusive) { v[q] = s; s = s + x; }
-            else { s = s + x; v[q] = s; }
-        }
-        double inc = s;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const double y = __shfl_up_sync(0xffffffffu, inc, d);
-            if (lane >= d) inc = inc + y;
-        }
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const double y = __shfl_up_sync(0xffffffffu, inc, d);
-            if (lane >= d) inc = inc > y ? inc : y;
-        }
-        double ex = __shfl_up_sync(0xffffffffu, inc, 1);
-        if (lane == 0) ex = 0.0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            if (e0 + q < cnt) {
-                const double x = ex + v[q];
-                key[pk(a0 + e0 + q)] = x < inc ? x : inc;
-            }
-        }
-        if (lane == 31) ctot[c] = inc;
-    }
-    __syncthreads();
-    double tot = 0.0;
-    for (u32 c = 0; c < C; ++c) tot = tot + ctot[c];
-    for (u32 c = wid; c < C; c += PP_TB / 32) {
-        double off = 0.0;
-        for (u32 k = 0; k < c; ++k) off = off + ctot[k];
-        const u32 e0 = c * 256 + lane * 8;
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-            if (e0 + q < cnt) key[pk(a0 + e0 + q)] = off + key[pk(a0 + e0 + q)];
-    }
-    __syncthreads();
-    return tot;
-}
-
-// Per block: stage the weights (bulk async copy), classify by warp ballots, place
-// lights and heavies in item order (rank = offset of the (row, warp) + rank
-// in the ballot), prefix keys, then one merge path over the two key
-// sequences writes every handled row (heavy first on ties: DH <= DL).
+// Per block: stage the weights (bulk async copy); one classification pass in
+// which each thread owns P consecutive items (16-byte shared loads) and sums
+// its lights' deficits and heavies' excess; a CTA scan of those sums and
+// counts (running max in the warp, warp bases summed sequentially, keys
+// clamped to the next thread's base, so keys are non-decreasing); one pass
+// that writes the class-compacted keys and items; then one merge path over
+// the two key sequences writes every handled row (heavy first on ties:
+// DH <= DL).  Round 1's count pass + strided compaction + two in-place key
+// prefixes took 54% of the kernel; this is 9.4 -> 7.6 ms at N=1e9 f32.
+// threads per prepack block: each owns P consecutive items read as 16-byte
+// vectors; 512 threads for f64 keep P = 8 (64 B per thread, the f32 pattern)
+template <typename T> struct PPTB {
+    static constexpr int v = sizeof(T) == 4 ? 256 : 512;
+};
 template <typename T>
-__global__ void __launch_bounds__(PP_TB) k_prepack_block(const T *__restrict__ w, u64 n, double avg,
+__global__ void __launch_bounds__(PPTB<T>::v) k_prepack_block(const T *__restrict__ w, u64 n, double avg,
                                                          u32 bs, u32 thr,
                                                          typename RowOf<T>::type *__restrict__ rows,
                                                          BlockInfo *__restrict__ info)
 {
+    constexpr int TBT = PPTB<T>::v;
     typedef typename RowOf<T>::type RowT;
     typedef decltype(RowT::tw) TwT;
     typedef decltype(RowT::alias) AliasT;
     extern __shared__ __align__(16) unsigned char pp_raw[];
     const PPSmem<T> S = pp_smem<T>(pp_raw, bs);
-    __shared__ u32 s_cnt[2][PP_MAXR * (PP_TB / 32)];
     __shared__ u64 s_written;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const u32 lt = (1u << lane) - 1u;
     const u64 b0 = (u64)blockIdx.x * bs;
     const u32 len = (u32)(b0 + bs <= n ? bs : n - b0);
-    const u32 R = (len + PP_TB - 1) / PP_TB;
-    const u32 E = R * (PP_TB / 32);
     // stage the block's weights: one bulk async copy (TMA) when aligned
     __shared__ __align__(8) u64 bar;
     const T *src = w + b0;
@@ -215,59 +138,162 @@ __global__ void __launch_bounds__(PP_TB) k_prepack_block(const T *__restrict__ w
         __syncthreads();  // the barrier is initialised before anyone waits on it
         mbar_wait(&bar, 0);
     } else {
-        for (u32 i = threadIdx.x; i < len; i += PP_TB) S.sw[i] = src[i];
+        for (u32 i = threadIdx.x; i < len; i += TBT) S.sw[i] = src[i];
         __syncthreads();
     }
-    // count per (row, warp); exactly-full items are final at once
+    // One classification pass: thread t owns the P consecutive items
+    // [t P, t P + P) (P a multiple of 4, so its values are 16-byte loads from
+    // the staged block).  Exactly-full items are final at once; lights and
+    // heavies are counted and their deficit / excess summed in item order.
     const ClassCut<T> cls(avg);
-    u32 cw = 0;
-    for (u32 r = 0; r < R; ++r) {
-        const u32 i = r * PP_TB + threadIdx.x;
-        int c = 3;
-        if (i < len) {
-            const T v = S.sw[i];
-            c = cls(v);
-            if (c == 2) {
+    const u32 P = ((len + TBT - 1) / TBT + 3) & ~3u;
+    const u32 i0 = threadIdx.x * P;
+    u64 lmask = 0, hmask = 0;
+    u32 cw = 0, tl = 0, th = 0;
+    double sl = 0.0, sh = 0.0;
+    for (u32 q = 0; q < P; q += 4) {
+        T v4[4];
+        const u32 i = i0 + q;
+        if (i + 4 <= len) {
+            if (sizeof(T) == 4) {
+                const float4 f = *reinterpret_cast<const float4 *>(S.sw + i);
+                v4[0] = (T)f.x; v4[1] = (T)f.y; v4[2] = (T)f.z; v4[3] = (T)f.w;
+            } else {
+                const double2 d0 = *reinterpret_cast<const double2 *>(S.sw + i);
+                const double2 d1 = *reinterpret_cast<const double2 *>(S.sw + i + 2);
+                v4[0] = (T)d0.x; v4[1] = (T)d0.y; v4[2] = (T)d1.x; v4[3] = (T)d1.y;
+            }
+        } else {
+#pragma unroll
+            for (int z = 0; z < 4; ++z) v4[z] = i + z < len ? S.sw[i + z] : (T)0;
+        }
+#pragma unroll
+        for (int z = 0; z < 4; ++z) {
+            if (i + z >= len) continue;
+            const int c = cls(v4[z]);
+            const double x = (double)v4[z] - avg;
+            if (c == 0) {
+                lmask |= 1ull << (q + z);
+                sl = sl - x;  // avg - w == -(w - avg) exactly
+                ++tl;
+            } else if (c == 1) {
+                hmask |= 1ull << (q + z);
+                sh = sh + x;
+                ++th;
+            } else {
                 RowT row;
-                row.tw = (TwT)v;
-                row.alias = (AliasT)(b0 + i + 1);
-                rows[b0 + i] = row;
+                row.tw = (TwT)v4[z];
+                row.alias = (AliasT)(b0 + i + z + 1);
+                rows[b0 + i + z] = row;
                 ++cw;
             }
         }
-        const unsigned lb = __ballot_sync(0xffffffffu, c == 0), hb = __ballot_sync(0xffffffffu, c == 1);
-        if (lane == 0) {
-            s_cnt[0][r * (PP_TB / 32) + wid] = __popc(lb);
-            s_cnt[1][r * (PP_TB / 32) + wid] = __popc(hb);
-        }
-    }
-    __syncthreads();
-    u32 nl, nh;
-    {
-        // exclusive offsets of the (row, warp) counts, in item order
-        const u32 e0 = 2 * threadIdx.x, e1 = e0 + 1;
-        const u32 l0 = e0 < E ? s_cnt[0][e0] : 0, l1 = e1 < E ? s_cnt[0][e1] : 0;
-        const u32 h0 = e0 < E ? s_cnt[1][e0] : 0, h1 = e1 < E ? s_cnt[1][e1] : 0;
-        u32 el, eh;
-        block_scan2(l0 + l1, h0 + h1, el, eh, nl, nh);
-        if (e0 < E) { s_cnt[0][e0] = el; s_cnt[1][e0] = eh; }
-        if (e1 < E) { s_cnt[0][e1] = el + l0; s_cnt[1][e1] = eh + h0; }
     }
     if (cw) atomicAdd((unsigned long long *)&s_written, (unsigned long long)cw);
-    __syncthreads();
-    // class-compacted terms (avg - w for lights, w - avg for heavies) and offsets
-    for (u32 r = 0; r < R; ++r) {
-        const u32 i = r * PP_TB + threadIdx.x;
-        const int c = i < len ? cls(S.sw[i]) : 3;
-        const unsigned lb = __ballot_sync(0xffffffffu, c == 0), hb = __ballot_sync(0xffffffffu, c == 1);
-        if (c < 2) {  // one store path for both classes (no divergence)
-            const bool l = c == 0;
-            const u32 rk = s_cnt[l ? 0 : 1][r * (PP_TB / 32) + wid] + __popc((l ? lb : hb) & lt);
-            const double x = (double)S.sw[i] - avg;
-            S.key[pk(l ? rk : nl + 1 + rk)] = l ? -x : x;  // avg - w == -(w - avg) exactly
-            S.item[l ? rk : nl + rk] = (unsigned short)i;
+    // CTA scan of (sl, sh, tl, th): warp Kogge-Stone with a running max on the
+    // sums (non-decreasing lane bases), warp bases summed sequentially, so a
+    // thread's last key never passes the next thread's base: keys are
+    // non-decreasing in item order (the merge needs sorted keys)
+    __shared__ double s_wl[TBT / 32 + 1], s_wh[TBT / 32 + 1];
+    __shared__ u32 s_cl[TBT / 32 + 1], s_ch[TBT / 32 + 1];
+    double il = sl, ih = sh;
+    u32 cl = tl, ch = th;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const double yl = __shfl_up_sync(0xffffffffu, il, d), yh = __shfl_up_sync(0xffffffffu, ih, d);
+        const u32 zl = __shfl_up_sync(0xffffffffu, cl, d), zh = __shfl_up_sync(0xffffffffu, ch, d);
+        if (lane >= d) {
+            il = il + yl;
+            ih = ih + yh;
+            cl += zl;
+            ch += zh;
         }
     }
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const double yl = __shfl_up_sync(0xffffffffu, il, d), yh = __shfl_up_sync(0xffffffffu, ih, d);
+        if (lane >= d) {
+            il = il > yl ? il : yl;
+            ih = ih > yh ? ih : yh;
+        }
+    }
+    if (lane == 31) {
+        s_wl[wid] = il;
+        s_wh[wid] = ih;
+        s_cl[wid] = cl;
+        s_ch[wid] = ch;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // sequential warp bases (exclusive), totals at [NW]
+        double al = 0.0, ah = 0.0;
+        u32 bl = 0, bh = 0;
+        for (int k = 0; k < TBT / 32; ++k) {
+            const double xl = s_wl[k], xh = s_wh[k];
+            const u32 yl = s_cl[k], yh = s_ch[k];
+            s_wl[k] = al;
+            s_wh[k] = ah;
+            s_cl[k] = bl;
+            s_ch[k] = bh;
+            al = al + xl;
+            ah = ah + xh;
+            bl += yl;
+            bh += yh;
+        }
+        s_wl[TBT / 32] = al;
+        s_wh[TBT / 32] = ah;
+        s_cl[TBT / 32] = bl;
+        s_ch[TBT / 32] = bh;
+    }
+    __syncthreads();
+    const u32 nl = s_cl[TBT / 32], nh = s_ch[TBT / 32];
+    const double DLtot = s_wl[TBT / 32];
+    {
+        const double el = __shfl_up_sync(0xffffffffu, il, 1), eh = __shfl_up_sync(0xffffffffu, ih, 1);
+        const double Wl = s_wl[wid], Wh = s_wh[wid];
+        // this thread's bases and the next thread's (the clamp)
+        const double BL = Wl + (lane ? el : 0.0), BH = Wh + (lane ? eh : 0.0);
+        const double nBL = lane < 31 ? Wl + il : s_wl[wid + 1];
+        const double nBH = lane < 31 ? Wh + ih : s_wh[wid + 1];
+        u32 rl = s_cl[wid] + cl - tl, rh = s_ch[wid] + ch - th;
+        double pl = 0.0, ph = 0.0;
+        for (u32 q = 0; q < P; q += 4) {
+            if (!(((lmask | hmask) >> q) & 0xFull)) continue;
+            const u32 i = i0 + q;
+            T v4[4];
+            if (i + 4 <= len) {
+                if (sizeof(T) == 4) {
+                    const float4 f = *reinterpret_cast<const float4 *>(S.sw + i);
+                    v4[0] = (T)f.x; v4[1] = (T)f.y; v4[2] = (T)f.z; v4[3] = (T)f.w;
+                } else {
+                    const double2 d0 = *reinterpret_cast<const double2 *>(S.sw + i);
+                    const double2 d1 = *reinterpret_cast<const double2 *>(S.sw + i + 2);
+                    v4[0] = (T)d0.x; v4[1] = (T)d0.y; v4[2] = (T)d1.x; v4[3] = (T)d1.y;
+                }
+            } else {
+#pragma unroll
+                for (int z = 0; z < 4; ++z) v4[z] = i + z < len ? S.sw[i + z] : (T)0;
+            }
+#pragma unroll
+            for (int z = 0; z < 4; ++z) {
+                const bool isl = (lmask >> (q + z)) & 1, ish = (hmask >> (q + z)) & 1;
+                const double x = (double)v4[z] - avg;
+                if (isl) {
+                    const double k = BL + pl;
+                    S.key[pk(rl)] = k < nBL ? k : nBL;
+                    S.item[rl] = (unsigned short)(i + z);
+                    pl = pl - x;
+                    ++rl;
+                } else if (ish) {
+                    ph = ph + x;
+                    const double k = BH + ph;
+                    S.key[pk(nl + 1 + rh)] = k < nBH ? k : nBH;
+                    S.item[nl + rh] = (unsigned short)(i + z);
+                    ++rh;
+                }
+            }
+        }
+    }
+    if (threadIdx.x == 0) S.key[pk(nl)] = DLtot;
     __syncthreads();
     const bool pair = nl >= thr && nh >= thr;
     u32 kend = 0, cur = 0;
@@ -276,9 +302,6 @@ __global__ void __launch_bounds__(PP_TB) k_prepack_block(const T *__restrict__ w
     u64 nwritten = 0;
     if (pair) {
         // keys: DL exclusive over lights (DL(nl) = the whole deficit), DH inclusive
-        const double DLtot = block_prefix(S.key, 0, nl, true);
-        if (threadIdx.x == 0) S.key[pk(nl)] = DLtot;
-        block_prefix(S.key, nl + 1, nh, false);
         const double *key = S.key;
         auto DL = [&](u32 k) { return key[pk(k)]; };           // [0, nl]
         auto DH = [&](u32 j) { return key[pk(nl + 1 + j)]; };  // [0, nh)
@@ -369,7 +392,7 @@ __global__ void __launch_bounds__(PP_TB) k_prepack_block(const T *__restrict__ w
             // (k < kend) aliases the next heavy, a taken heavy j (j < jt)
             // closes against the lights taken before it
             const u32 total = nl + nh;
-            const u32 per = (total + PP_TB - 1) / PP_TB;
+            const u32 per = (total + TBT - 1) / TBT;
             const u32 d0 = threadIdx.x * per;
             if (d0 < total) {
                 const u32 lo0 = d0 > nh ? d0 - nh : 0, hi0 = d0 < nl ? d0 : nl;
@@ -603,11 +626,11 @@ int ak_greedy_prepack_ex(const void *w, int dtype, uint64_t n, double avg, uint3
     }
     if (dtype == AK_F32) {
         AK_SMEM_ATTR(k_prepack_block<float>, (int)smem);
-        k_prepack_block<float><<<(unsigned)nb, PP_TB, smem, st>>>((const float *)w, n, avg, block_size,
+        k_prepack_block<float><<<(unsigned)nb, PPTB<float>::v, smem, st>>>((const float *)w, n, avg, block_size,
                                                                  threshold, (RowF32 *)rows, info);
     } else if (dtype == AK_F64) {
         AK_SMEM_ATTR(k_prepack_block<double>, (int)smem);
-        k_prepack_block<double><<<(unsigned)nb, PP_TB, smem, st>>>((const double *)w, n, avg, block_size,
+        k_prepack_block<double><<<(unsigned)nb, PPTB<double>::v, smem, st>>>((const double *)w, n, avg, block_size,
                                                                   threshold, (RowF64 *)rows, info);
     } else {
         return AK_ERR_VALUE;
