@@ -507,25 +507,87 @@ __global__ void __launch_bounds__(PP_TB) k_prepack_emit(const T *__restrict__ w,
     }
 }
 
-__global__ void k_info_to_counts(const BlockInfo *info, u64 nb, i64 *cnt, unsigned long long *nw)
+// Block-count scan, multi-CTA: each CTA of PPS_T threads owns PPS_CHUNK
+// consecutive blocks.  k_pp_partials sums a chunk's residual counts (and adds
+// its written pairs into *nw, one atomic per CTA); k_excl_scan_i64 scans the
+// chunk sums; k_pp_offsets rescans each chunk from its base.
+constexpr int PPS_T = 256, PPS_PER = 8, PPS_CHUNK = PPS_T * PPS_PER;
+
+__device__ __forceinline__ i64 pps_block_sum(i64 v, i64 *ws)
 {
-    const u64 b = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nb) return;
-    cnt[b] = info[b].nres;
-    atomicAdd(nw, (unsigned long long)info[b].nwritten);
+    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+    __syncthreads();
+    i64 t = 0;
+#pragma unroll
+    for (int k = 0; k < PPS_T / 32; ++k) t += ws[k];
+    return t;
 }
 
-// exclusive scan of block counts (single CTA, sequential chunks)
+__global__ void __launch_bounds__(PPS_T) k_pp_partials(const BlockInfo *__restrict__ info, u64 nb,
+                                                       i64 *__restrict__ part,
+                                                       unsigned long long *nw)
+{
+    __shared__ i64 ws0[PPS_T / 32], ws1[PPS_T / 32];
+    const u64 c0 = (u64)blockIdx.x * PPS_CHUNK;
+    i64 r = 0, w = 0;
+#pragma unroll
+    for (int k = 0; k < PPS_PER; ++k) {
+        const u64 b = c0 + (u64)k * PPS_T + threadIdx.x;
+        if (b < nb) {
+            r += info[b].nres;
+            w += info[b].nwritten;
+        }
+    }
+    r = pps_block_sum(r, ws0);
+    w = pps_block_sum(w, ws1);
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = r;
+        if (w) atomicAdd(nw, (unsigned long long)w);
+    }
+}
+
+__global__ void __launch_bounds__(PPS_T) k_pp_offsets(const BlockInfo *__restrict__ info, u64 nb,
+                                                      const i64 *__restrict__ part_off,
+                                                      i64 *__restrict__ off)
+{
+    __shared__ i64 ws[PPS_T / 32];
+    const u64 b0 = (u64)blockIdx.x * PPS_CHUNK + (u64)threadIdx.x * PPS_PER;
+    i64 v[PPS_PER], s = 0;
+#pragma unroll
+    for (int k = 0; k < PPS_PER; ++k) {
+        v[k] = b0 + k < nb ? info[b0 + k].nres : 0;
+        s += v[k];
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    i64 inc = s;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const i64 y = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += y;
+    }
+    if (lane == 31) ws[wid] = inc;
+    __syncthreads();
+    i64 ex = part_off[blockIdx.x] + inc - s;
+    for (int k = 0; k < wid; ++k) ex += ws[k];
+#pragma unroll
+    for (int k = 0; k < PPS_PER; ++k) {
+        if (b0 + k < nb) off[b0 + k] = ex;
+        ex += v[k];
+    }
+}
+
+// exclusive scan of chunk sums (single CTA, sequential chunks; a few hundred
+// values for N=1e9)
 __global__ void k_excl_scan_i64(const i64 *cnt, u64 nb, i64 *off, i64 *total)
 {
     __shared__ i64 carry;
+    __shared__ i64 ws[32];
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
     for (u64 base = 0; base < nb; base += blockDim.x) {
         const u64 b = base + threadIdx.x;
         const i64 v = b < nb ? cnt[b] : 0;
-        // warp + block inclusive scan
-        __shared__ i64 ws[32];
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
         i64 inc = v;
         for (int d = 1; d < 32; d <<= 1) {
@@ -636,10 +698,17 @@ int ak_greedy_prepack_ex(const void *w, int dtype, uint64_t n, double avg, uint3
         return AK_ERR_VALUE;
     }
     AK_LAUNCH_CHECK("k_prepack_block");
-    k_info_to_counts<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(info, nb, cnt, nw);
-    AK_LAUNCH_CHECK("k_info_to_counts");
-    k_excl_scan_i64<<<1, 1024, 0, st>>>(cnt, nb, off, tot);
-    AK_LAUNCH_CHECK("k_excl_scan_i64");
+    {
+        // chunk sums in cnt[0, G), their exclusive scan in cnt[G, 2G)
+        // (2G <= nb + 1 slots for every nb >= 1)
+        const u64 G = (nb + PPS_CHUNK - 1) / PPS_CHUNK;
+        k_pp_partials<<<(unsigned)G, PPS_T, 0, st>>>(info, nb, cnt, nw);
+        AK_LAUNCH_CHECK("k_pp_partials");
+        k_excl_scan_i64<<<1, 1024, 0, st>>>(cnt, G, cnt + G, tot);
+        AK_LAUNCH_CHECK("k_excl_scan_i64");
+        k_pp_offsets<<<(unsigned)G, PPS_T, 0, st>>>(info, nb, cnt + G, off);
+        AK_LAUNCH_CHECK("k_pp_offsets");
+    }
     if (dtype == AK_F32)
         k_prepack_emit<float><<<(unsigned)nb, PP_TB, 0, st>>>((const float *)w, n, avg, block_size, info,
                                                              off, res_idx, res_w);
