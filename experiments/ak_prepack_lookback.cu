@@ -1,3 +1,8 @@
+// EXPERIMENT (not compiled into libaliaskit_b200.so): PSA+ prepack with the
+// residual emitted inside k_prepack_block, each block finding its residual
+// offset by a decoupled look-back over per-block residual counts (warp 0 as a
+// dedicated look-back warp).  Passes tests/test_gpu_prepack.py, but is slower
+// than the product's prepack + warp-per-block emit; see experiments/README.md.
 // ak_prepack.cu — PSA+ (greedy block-local prepack, partition.py:134-282, and
 // psa_plus_construct, pack.py:280-305) on the device.
 //
@@ -20,26 +25,19 @@
 // with the reference's f64 chain except at ties inside its rounding noise.
 //
 //   k_prepack_block   classify (thread = P consecutive items), CTA scan,
-//                     compacted keys, merge, handled rows, per-block residual
-//                     summary
-//   k_prepack_emit    residual items (index, weight) in global item order
+//                     compacted keys, merge, handled rows; the block's
+//                     residual offset by decoupled look-back over the blocks
+//                     before it, then its residual items (index, weight) in
+//                     global item order
 //   k_residual_remap  the residual table (built by the fused builder with the
 //                     global average) scattered into the final table
 #include "ak_common.cuh"
 
 namespace {
 
-struct BlockInfo {
-    u32 nl, nh;     // lights / heavies of the block
-    u32 kend;       // lights [0, kend) handled
-    int jt;         // terminal heavy (-1: no pairing); heavies (jt, nh) forwarded
-    u32 cur;        // 1: heavy jt forwarded with residual curw
-    u32 nres;       // forwarded items
-    u32 pL, pH;     // block offsets of the first forwarded light / heavy (len: none)
-    u32 pT;         // block offset of the forwarded terminal heavy (~0: none)
-    double curw;
-    u64 nwritten;   // rows written by the block
-};
+// per-block residual status words for the look-back: flag in the top two
+// bits (1: the block's own count, 2: inclusive prefix), value below
+constexpr u64 PP_AGG = 1ull << 62, PP_INC = 2ull << 62, PP_VAL = PP_AGG - 1;
 
 template <typename T> __device__ __forceinline__ int item_class(T v, double avg)
 {
@@ -105,7 +103,10 @@ template <typename T>
 __global__ void __launch_bounds__(PPTB<T>::v) k_prepack_block(const T *__restrict__ w, u64 n, double avg,
                                                          u32 bs, u32 thr,
                                                          typename RowOf<T>::type *__restrict__ rows,
-                                                         BlockInfo *__restrict__ info)
+                                                         u64 *__restrict__ status,
+                                                         i64 *__restrict__ res_idx,
+                                                         double *__restrict__ res_w,
+                                                         unsigned long long *nw, i64 *tot)
 {
     constexpr int TBT = PPTB<T>::v;
     typedef typename RowOf<T>::type RowT;
@@ -115,7 +116,6 @@ __global__ void __launch_bounds__(PPTB<T>::v) k_prepack_block(const T *__restric
     const PPSmem<T> S = pp_smem<T>(pp_raw, bs);
     __shared__ u64 s_written;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const u32 lt = (1u << lane) - 1u;
     const u64 b0 = (u64)blockIdx.x * bs;
     const u32 len = (u32)(b0 + bs <= n ? bs : n - b0);
     // stage the block's weights: one bulk async copy (TMA) when aligned
@@ -165,20 +165,20 @@ __global__ void __launch_bounds__(PPTB<T>::v) k_prepack_block(const T *__restric
 #pragma unroll
             for (int z = 0; z < 4; ++z) v4[z] = i + z < len ? S.sw[i + z] : (T)0;
         }
-        // branch-free (classes are random per lane): adding an exact 0.0
-        // leaves a sum unchanged, so the sums equal the per-class chains
-        u32 l4 = 0, h4 = 0;
 #pragma unroll
         for (int z = 0; z < 4; ++z) {
-            const bool in = i + z < len;
+            if (i + z >= len) continue;
             const int c = cls(v4[z]);
-            const bool L = in && c == 0, H = in && c == 1;
             const double x = (double)v4[z] - avg;
-            sl = sl - (L ? x : 0.0);  // avg - w == -(w - avg) exactly
-            sh = sh + (H ? x : 0.0);
-            l4 |= (u32)L << z;
-            h4 |= (u32)H << z;
-            if (in && c == 2) {  // exactly full: final at once (rare)
+            if (c == 0) {
+                lmask |= 1ull << (q + z);
+                sl = sl - x;  // avg - w == -(w - avg) exactly
+                ++tl;
+            } else if (c == 1) {
+                hmask |= 1ull << (q + z);
+                sh = sh + x;
+                ++th;
+            } else {
                 RowT row;
                 row.tw = (TwT)v4[z];
                 row.alias = (AliasT)(b0 + i + z + 1);
@@ -186,11 +186,7 @@ __global__ void __launch_bounds__(PPTB<T>::v) k_prepack_block(const T *__restric
                 ++cw;
             }
         }
-        lmask |= (u64)l4 << q;
-        hmask |= (u64)h4 << q;
     }
-    tl = __popcll(lmask);
-    th = __popcll(hmask);
     if (cw) atomicAdd((unsigned long long *)&s_written, (unsigned long long)cw);
     // CTA scan of (sl, sh, tl, th): warp Kogge-Stone with a running max on the
     // sums (non-decreasing lane bases), warp bases summed sequentially, so a
@@ -275,22 +271,23 @@ __global__ void __launch_bounds__(PPTB<T>::v) k_prepack_block(const T *__restric
 #pragma unroll
                 for (int z = 0; z < 4; ++z) v4[z] = i + z < len ? S.sw[i + z] : (T)0;
             }
-            const u32 l4 = (u32)(lmask >> q) & 0xFu, h4 = (u32)(hmask >> q) & 0xFu;
 #pragma unroll
             for (int z = 0; z < 4; ++z) {
-                // branch-free, as the classification pass
-                const bool isl = (l4 >> z) & 1, ish = (h4 >> z) & 1;
+                const bool isl = (lmask >> (q + z)) & 1, ish = (hmask >> (q + z)) & 1;
                 const double x = (double)v4[z] - avg;
-                ph = ph + (ish ? x : 0.0);
-                const double k = isl ? BL + pl : BH + ph;
-                const double cap = isl ? nBL : nBH;
-                if (isl || ish) {
-                    S.key[pk(isl ? rl : nl + 1 + rh)] = k < cap ? k : cap;
-                    S.item[isl ? rl : nl + rh] = (unsigned short)(i + z);
+                if (isl) {
+                    const double k = BL + pl;
+                    S.key[pk(rl)] = k < nBL ? k : nBL;
+                    S.item[rl] = (unsigned short)(i + z);
+                    pl = pl - x;
+                    ++rl;
+                } else if (ish) {
+                    ph = ph + x;
+                    const double k = BH + ph;
+                    S.key[pk(nl + 1 + rh)] = k < nBH ? k : nBH;
+                    S.item[nl + rh] = (unsigned short)(i + z);
+                    ++rh;
                 }
-                pl = pl - (isl ? x : 0.0);
-                rl += isl;
-                rh += ish;
             }
         }
     }
@@ -301,6 +298,41 @@ __global__ void __launch_bounds__(PPTB<T>::v) k_prepack_block(const T *__restric
     int jt = -1;
     double curw = 0.0;
     u64 nwritten = 0;
+    // The block's residual offset.  Warp 0 is the look-back warp: as soon as
+    // the pairing is decided it publishes the block's residual count, walks
+    // back over the blocks before it 32 status words at a time (waiting on
+    // any not yet published) and publishes the inclusive prefix, while warps
+    // 1.. run the merge path.  Counts are published before the merge, so the
+    // walk rarely waits and inclusive prefixes appear early, which keeps it
+    // short.  Blocks start in index order (as for the builder's scan), so
+    // every predecessor is running or done.  The status words carry their own
+    // values: relaxed loads and stores, no fences.
+    __shared__ i64 s_roff;
+    auto lookback = [&](u32 nr) {  // warp 0
+        const u64 me = blockIdx.x;
+        if (lane == 0) st_relaxed_u64(&status[me], (me == 0 ? PP_INC : PP_AGG) | nr);
+        i64 excl = 0;
+        for (i64 pred = (i64)me - 1; pred >= 0; pred -= 32) {
+            const i64 p = pred - lane;
+            u64 sw = PP_INC;  // before block 0: an inclusive prefix of 0
+            if (p >= 0) {
+                do { sw = ld_relaxed_u64(&status[p]); } while ((sw >> 62) == 0);
+            }
+            const unsigned inc = __ballot_sync(0xffffffffu, (sw >> 62) == 2);
+            const int stop = inc ? __ffs(inc) - 1 : 32;
+            i64 c = lane <= stop ? (i64)(sw & PP_VAL) : 0;
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) c += __shfl_xor_sync(0xffffffffu, c, m);
+            excl += c;
+            if (stop < 32) break;
+        }
+        if (lane == 0) {
+            if (me > 0) st_relaxed_u64(&status[me], PP_INC | (u64)(excl + nr));
+            if (me + 1 == gridDim.x) *tot = excl + nr;
+            s_roff = excl;
+        }
+    };
+    if (!pair && wid == 0) lookback(nl + nh);
     if (pair) {
         // keys: DL exclusive over lights (DL(nl) = the whole deficit), DH inclusive
         const double *key = S.key;
@@ -387,14 +419,17 @@ __global__ void __launch_bounds__(PPTB<T>::v) k_prepack_block(const T *__restric
             jt = s_j;
             cur = s_cur;
             curw = s_w;
+            if (wid == 0) lookback((nl - kend) + (u32)((int)nh - (jt + 1)) + cur);
+        } else if (wid == 0) {
+            lookback((nl - kend) + (u32)((int)nh - (jt + 1)) + cur);
         } else {
-            // merge path over lights [0, nl) and heavies [0, nh): thread t
-            // takes merged positions [t per, (t + 1) per); a taken light k
-            // (k < kend) aliases the next heavy, a taken heavy j (j < jt)
-            // closes against the lights taken before it
+            // merge path over lights [0, nl) and heavies [0, nh): merge
+            // thread t (warps 1..) takes merged positions [t per, (t + 1)
+            // per); a taken light k (k < kend) aliases the next heavy, a taken
+            // heavy j (j < jt) closes against the lights taken before it
             const u32 total = nl + nh;
-            const u32 per = (total + TBT - 1) / TBT;
-            const u32 d0 = threadIdx.x * per;
+            const u32 per = (total + (TBT - 32) - 1) / (TBT - 32);
+            const u32 d0 = (threadIdx.x - 32) * per;
             if (d0 < total) {
                 const u32 lo0 = d0 > nh ? d0 - nh : 0, hi0 = d0 < nl ? d0 : nl;
                 u32 lo = lo0, hi = hi0;  // greatest i with light i-1 before heavy d0-i
@@ -430,7 +465,7 @@ __global__ void __launch_bounds__(PPTB<T>::v) k_prepack_block(const T *__restric
                     }
                 }
             }
-            if (threadIdx.x == 0 && !cur) {
+            if (threadIdx.x == 32 && !cur) {
                 const u64 it = b0 + S.item[nl + jt];
                 RowT row;
                 row.tw = tw_store<T>(wt_end, avg);
@@ -441,175 +476,49 @@ __global__ void __launch_bounds__(PPTB<T>::v) k_prepack_block(const T *__restric
         nwritten = (u64)kend + (u64)jt + (cur ? 0 : 1);
     }
     __syncthreads();
+    // Forwarded items: the lights from rank kend and the heavies from rank hf
+    // (the terminal heavy jt itself when it carries a residual), in item order.
+    const u32 nres = (nl - kend) + (u32)((int)nh - (jt + 1)) + (pair ? cur : 0u);
+    const u32 hf = (u32)(jt + 1) - (pair && cur ? 1u : 0u);
     if (threadIdx.x == 0) {
-        BlockInfo bi;
-        bi.nl = nl;
-        bi.nh = nh;
-        bi.kend = kend;
-        bi.jt = jt;
-        bi.cur = pair ? cur : 0u;
-        bi.curw = curw;
-        bi.nres = (nl - kend) + (u32)((int)nh - (jt + 1)) + (pair ? cur : 0u);
-        bi.nwritten = s_written + nwritten;
-        // forwarded items: the lights from rank kend and the heavies from
-        // rank jt + 1 (jt itself when it carries a residual), in item order
-        const u32 hf = (u32)(jt + 1) - (pair && cur ? 1u : 0u);
-        bi.pL = kend < nl ? S.item[kend] : len;
-        bi.pH = hf < nh ? S.item[nl + hf] : len;
-        bi.pT = pair && cur ? S.item[nl + jt] : 0xFFFFFFFFu;
-        info[blockIdx.x] = bi;
+        const u64 wr = s_written + nwritten;
+        if (wr) atomicAdd(nw, (unsigned long long)wr);
     }
-}
-
-// Residual items of each block in item order at res_off[block] + ...: the
-// lights at block offsets >= pL and the heavies at offsets >= pH (the
-// terminal heavy at pT with its residual weight), i.e. only the block's tail
-// from min(pL, pH) is visited.  One warp per block (PE_WARPS blocks per CTA)
-// with 128 items in flight per step: the pass is latency-bound (info ->
-// offset -> tail loads), and a CTA per block with barriers between 256-item
-// steps left most of that latency exposed.
-constexpr int PE_WARPS = 8;
-template <typename T>
-__global__ void __launch_bounds__(PE_WARPS * 32) k_prepack_emit(const T *__restrict__ w, u64 n, double avg,
-                                                             u32 bs, u64 nb,
-                                                             const BlockInfo *__restrict__ info,
-                                                             const i64 *__restrict__ res_off,
-                                                             i64 *__restrict__ res_idx,
-                                                             double *__restrict__ res_w)
-{
-    const int lane = threadIdx.x & 31;
-    const u64 b = (u64)blockIdx.x * PE_WARPS + (threadIdx.x >> 5);
-    if (b >= nb) return;
-    const BlockInfo bi = info[b];
-    if (bi.nres == 0) return;
-    const u64 b0 = b * bs;
-    const u32 len = (u32)(b0 + bs <= n ? bs : n - b0);
-    const u32 lt = (1u << lane) - 1u;
-    i64 pos = res_off[b];
-    for (u32 base = bi.pL < bi.pH ? bi.pL : bi.pH; base < len; base += 128) {
-        T v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const u32 i = base + u * 32 + lane;
-            v[u] = i < len ? w[b0 + i] : T(0);
+    if (nres == 0) return;
+    // the residual items: lights at block offsets >= pL, heavies at offsets
+    // >= pH (the terminal heavy at pT with its residual weight), so only the
+    // block's tail from min(pL, pH) is visited, TBT items per step
+    const u32 pL = kend < nl ? S.item[kend] : len;
+    const u32 pH = hf < nh ? S.item[nl + hf] : len;
+    const u32 pT = pair && cur ? S.item[nl + jt] : 0xFFFFFFFFu;
+    __shared__ u32 s_fw[TBT / 32];
+    i64 pos = s_roff;
+    for (u32 base = pL < pH ? pL : pH; base < len; base += TBT) {
+        const u32 i = base + threadIdx.x;
+        bool f = false;
+        T v = T(0);
+        if (i < len) {
+            v = S.sw[i];
+            const int c = cls(v);
+            f = (c == 0 && i >= pL) || (c == 1 && i >= pH);
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const u32 i = base + u * 32 + lane;
-            bool f = false;
-            if (i < len) {
-                const int c = item_class(v[u], avg);
-                f = (c == 0 && i >= bi.pL) || (c == 1 && i >= bi.pH);
-            }
-            const unsigned fb = __ballot_sync(0xffffffffu, f);
-            if (f) {
-                const i64 q = pos + __popc(fb & lt);
-                res_idx[q] = (i64)(b0 + i + 1);
-                res_w[q] = i == bi.pT ? bi.curw : (double)v[u];
-            }
-            pos += __popc(fb);
-        }
-    }
-}
-
-// Block-count scan, multi-CTA: each CTA of PPS_T threads owns PPS_CHUNK
-// consecutive blocks.  k_pp_partials sums a chunk's residual counts (and adds
-// its written pairs into *nw, one atomic per CTA); k_excl_scan_i64 scans the
-// chunk sums; k_pp_offsets rescans each chunk from its base.
-constexpr int PPS_T = 256, PPS_PER = 8, PPS_CHUNK = PPS_T * PPS_PER;
-
-__device__ __forceinline__ i64 pps_block_sum(i64 v, i64 *ws)
-{
-    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
-    __syncthreads();
-    i64 t = 0;
-#pragma unroll
-    for (int k = 0; k < PPS_T / 32; ++k) t += ws[k];
-    return t;
-}
-
-__global__ void __launch_bounds__(PPS_T) k_pp_partials(const BlockInfo *__restrict__ info, u64 nb,
-                                                       i64 *__restrict__ part,
-                                                       unsigned long long *nw)
-{
-    __shared__ i64 ws0[PPS_T / 32], ws1[PPS_T / 32];
-    const u64 c0 = (u64)blockIdx.x * PPS_CHUNK;
-    i64 r = 0, w = 0;
-#pragma unroll
-    for (int k = 0; k < PPS_PER; ++k) {
-        const u64 b = c0 + (u64)k * PPS_T + threadIdx.x;
-        if (b < nb) {
-            r += info[b].nres;
-            w += info[b].nwritten;
-        }
-    }
-    r = pps_block_sum(r, ws0);
-    w = pps_block_sum(w, ws1);
-    if (threadIdx.x == 0) {
-        part[blockIdx.x] = r;
-        if (w) atomicAdd(nw, (unsigned long long)w);
-    }
-}
-
-__global__ void __launch_bounds__(PPS_T) k_pp_offsets(const BlockInfo *__restrict__ info, u64 nb,
-                                                      const i64 *__restrict__ part_off,
-                                                      i64 *__restrict__ off)
-{
-    __shared__ i64 ws[PPS_T / 32];
-    const u64 b0 = (u64)blockIdx.x * PPS_CHUNK + (u64)threadIdx.x * PPS_PER;
-    i64 v[PPS_PER], s = 0;
-#pragma unroll
-    for (int k = 0; k < PPS_PER; ++k) {
-        v[k] = b0 + k < nb ? info[b0 + k].nres : 0;
-        s += v[k];
-    }
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    i64 inc = s;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const i64 y = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += y;
-    }
-    if (lane == 31) ws[wid] = inc;
-    __syncthreads();
-    i64 ex = part_off[blockIdx.x] + inc - s;
-    for (int k = 0; k < wid; ++k) ex += ws[k];
-#pragma unroll
-    for (int k = 0; k < PPS_PER; ++k) {
-        if (b0 + k < nb) off[b0 + k] = ex;
-        ex += v[k];
-    }
-}
-
-// exclusive scan of chunk sums (single CTA, sequential chunks; a few hundred
-// values for N=1e9)
-__global__ void k_excl_scan_i64(const i64 *cnt, u64 nb, i64 *off, i64 *total)
-{
-    __shared__ i64 carry;
-    __shared__ i64 ws[32];
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (u64 base = 0; base < nb; base += blockDim.x) {
-        const u64 b = base + threadIdx.x;
-        const i64 v = b < nb ? cnt[b] : 0;
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        i64 inc = v;
-        for (int d = 1; d < 32; d <<= 1) {
-            const i64 y = __shfl_up_sync(0xffffffffu, inc, d);
-            if (lane >= d) inc += y;
-        }
-        if (lane == 31) ws[wid] = inc;
+        const unsigned fb = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) s_fw[wid] = __popc(fb);
         __syncthreads();
-        i64 wo = 0;
-        for (int k = 0; k < wid; ++k) wo += ws[k];
-        const i64 ex = carry + wo + inc - v;
-        if (b < nb) off[b] = ex;
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry = ex + v;
+        u32 before = 0, all = 0;
+#pragma unroll
+        for (int k = 0; k < TBT / 32; ++k) {
+            before += k < wid ? s_fw[k] : 0u;
+            all += s_fw[k];
+        }
+        if (f) {
+            const i64 q = pos + before + __popc(fb & ((1u << lane) - 1u));
+            res_idx[q] = (i64)(b0 + i + 1);
+            res_w[q] = i == pT ? curw : (double)v;
+        }
+        pos += all;
         __syncthreads();
     }
-    if (threadIdx.x == 0) *total = carry;
 }
 
 // residual table (f64 rows over residual positions) -> final rows; with
@@ -652,7 +561,7 @@ extern "C" {
 size_t ak_prepack_workspace_bytes(uint64_t n, uint32_t block_size)
 {
     const u64 nb = block_size ? (n + block_size - 1) / block_size : 0;
-    return al256(nb * sizeof(BlockInfo)) + 2 * al256((nb + 1) * 8) + 256;
+    return al256(nb * 8) + 256;
 }
 
 int ak_greedy_prepack(const void *w, int dtype, uint64_t n, double avg, uint32_t block_size,
@@ -677,53 +586,29 @@ int ak_greedy_prepack_ex(const void *w, int dtype, uint64_t n, double avg, uint3
     cudaStream_t st = ak_stream(stream);
     const u64 nb = (n + block_size - 1) / block_size;
     char *p = (char *)ws;
-    BlockInfo *info = (BlockInfo *)p;
-    p += al256(nb * sizeof(BlockInfo));
-    i64 *cnt = (i64 *)p;
-    p += al256((nb + 1) * 8);
-    i64 *off = (i64 *)p;
-    p += al256((nb + 1) * 8);
+    u64 *status = (u64 *)p;
+    p += al256(nb * 8);
     unsigned long long *nw = (unsigned long long *)p;
     i64 *tot = (i64 *)(p + 64);
     const size_t rb = dtype == AK_F32 ? 8 : 16;
     if (clear_rows) AK_CUDA_TRY(cudaMemsetAsync(rows, 0, n * rb, st));
     {
-        const int rc0 = ak_fill_small(nw, 0, 8, st);
+        // the status words and the written count, one fill (they are adjacent)
+        const int rc0 = ak_fill_small(status, 0, al256(nb * 8) + 8, st);
         if (rc0 != AK_OK) return rc0;
     }
     if (dtype == AK_F32) {
         AK_SMEM_ATTR(k_prepack_block<float>, (int)smem);
-        k_prepack_block<float><<<(unsigned)nb, PPTB<float>::v, smem, st>>>((const float *)w, n, avg, block_size,
-                                                                 threshold, (RowF32 *)rows, info);
+        k_prepack_block<float><<<(unsigned)nb, PPTB<float>::v, smem, st>>>(
+            (const float *)w, n, avg, block_size, threshold, (RowF32 *)rows, status, res_idx, res_w, nw, tot);
     } else if (dtype == AK_F64) {
         AK_SMEM_ATTR(k_prepack_block<double>, (int)smem);
-        k_prepack_block<double><<<(unsigned)nb, PPTB<double>::v, smem, st>>>((const double *)w, n, avg, block_size,
-                                                                  threshold, (RowF64 *)rows, info);
+        k_prepack_block<double><<<(unsigned)nb, PPTB<double>::v, smem, st>>>(
+            (const double *)w, n, avg, block_size, threshold, (RowF64 *)rows, status, res_idx, res_w, nw, tot);
     } else {
         return AK_ERR_VALUE;
     }
     AK_LAUNCH_CHECK("k_prepack_block");
-    {
-        // chunk sums in cnt[0, G), their exclusive scan in cnt[G, 2G)
-        // (2G <= nb + 1 slots for every nb >= 1)
-        const u64 G = (nb + PPS_CHUNK - 1) / PPS_CHUNK;
-        k_pp_partials<<<(unsigned)G, PPS_T, 0, st>>>(info, nb, cnt, nw);
-        AK_LAUNCH_CHECK("k_pp_partials");
-        k_excl_scan_i64<<<1, 1024, 0, st>>>(cnt, G, cnt + G, tot);
-        AK_LAUNCH_CHECK("k_excl_scan_i64");
-        k_pp_offsets<<<(unsigned)G, PPS_T, 0, st>>>(info, nb, cnt + G, off);
-        AK_LAUNCH_CHECK("k_pp_offsets");
-    }
-    {
-        const unsigned g = (unsigned)((nb + PE_WARPS - 1) / PE_WARPS);
-        if (dtype == AK_F32)
-            k_prepack_emit<float><<<g, PE_WARPS * 32, 0, st>>>((const float *)w, n, avg, block_size, nb,
-                                                              info, off, res_idx, res_w);
-        else
-            k_prepack_emit<double><<<g, PE_WARPS * 32, 0, st>>>((const double *)w, n, avg, block_size, nb,
-                                                               info, off, res_idx, res_w);
-    }
-    AK_LAUNCH_CHECK("k_prepack_emit");
     i64 nres = 0;
     unsigned long long nwr = 0;
     {

@@ -199,6 +199,18 @@ int ak_greedy_prepack_ex(const void *w, int dtype, uint64_t n, double avg, uint3
  * table. */
 int ak_residual_scatter_count(const void *res_rows, const int64_t *res_idx, uint64_t nres,
                               double avg, int dtype, void *rows, uint64_t *written, void *stream);
+/* PSA+'s residual construction (pack.py:296-305: the forwarded items go
+ * through PSA with the global average) fused with the scatter: the k residual
+ * weights res_w (f64, 16-byte aligned, in item order) are built as by
+ * ak_build_psa_avg, and each residual row r is written straight into the
+ * final table `rows` (out_dtype AK_F32 / AK_F64) at res_idx[r] - 1 with alias
+ * res_idx[alias - 1], thresholds rounded as ak_residual_scatter rounds them.
+ * *written = the rows written (k when every residual bucket is filled).
+ * Equals ak_build_psa_avg + ak_residual_scatter_count without the
+ * intermediate residual table.  ws: ak_build_workspace_bytes(k, AK_F64). */
+int ak_build_psa_residual(const double *res_w, uint64_t k, double avg, const int64_t *res_idx,
+                          int out_dtype, void *rows, uint64_t *written, void *ws, size_t ws_bytes,
+                          void *stream);
 
 /* ---- sampling (sample.py) ----------------------------------------------- */
 

@@ -53,6 +53,7 @@ _SIGS = {
                                sz, vp]),
     "ak_residual_scatter": (ci, [vp, vp, u64, dbl, ci, vp, vp]),
     "ak_residual_scatter_count": (ci, [vp, vp, u64, dbl, ci, vp, vp, vp]),
+    "ak_build_psa_residual": (ci, [vp, u64, dbl, vp, ci, vp, vp, vp, sz, vp]),
     "ak_greedy_prepack_ex": (ci, [vp, ci, u64, dbl, C.c_uint32, C.c_uint32, ci, vp, vp, vp, vp, vp, vp,
                                   sz, vp]),
     "ak_sample_naive": (ci, [vp, ci, u64, dbl, u64, u64, u64, u64, u64, u64, vp, ci, vp]),

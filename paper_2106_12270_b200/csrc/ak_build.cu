@@ -841,14 +841,46 @@ __device__ __forceinline__ void chunk_ranks(const BuildWs &W, u64 n, u64 g0, int
     hb = g < nch ? base + (inc - hc) : ~0ull;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(TB, 5) k_build_pack(const T *__restrict__ w, u64 n, double avg,
-                                                      BuildWs W, SplitOut O,
-                                                      typename RowOf<T>::type *__restrict__ rows)
-{
+// Where the pack's rows go.  RowSink: row i of the table being built.
+// RemapSink (PSA+'s residual build, T = double): the residual table's row r is
+// the final table's row res_idx[r] - 1 and alias a its item res_idx[a - 1], so
+// the residual rows land in the final table directly (thresholds rounded to
+// the final table's type as ak_residual_scatter does), counting the rows.
+template <typename T> struct RowSink {
     typedef typename RowOf<T>::type RowT;
     typedef decltype(RowT::tw) TwT;
-    typedef decltype(RowT::alias) AliasT;
+    RowT *rows;
+    __device__ __forceinline__ void put(u64 pos, TwT tw, u64 al) const
+    {
+        RowT r;
+        r.tw = tw;
+        r.alias = (decltype(RowT::alias))al;
+        rows[pos] = r;
+    }
+    static constexpr bool counts = false;
+};
+template <typename RowOut> struct RemapSink {
+    typedef double TwT;
+    RowOut *rows;
+    const i64 *res_idx;
+    double avg;
+    unsigned long long *written;
+    __device__ __forceinline__ void put(u64 pos, double tw, u64 al) const
+    {
+        RowOut o;
+        o.tw = tw_store<decltype(RowOut::tw)>(tw, avg);
+        o.alias = al ? (decltype(RowOut::alias))res_idx[al - 1] : (decltype(RowOut::alias))0;
+        rows[res_idx[pos] - 1] = o;
+    }
+    static constexpr bool counts = true;
+};
+
+template <typename T, typename Sink>
+__global__ void __launch_bounds__(TB, 5) k_build_pack(const T *__restrict__ w, u64 n, double avg,
+                                                      BuildWs W, SplitOut O, Sink sink)
+{
+    typedef typename Sink::TwT TwT;
+    u32 nput = 0;  // rows written by this thread (RemapSink counts them)
     extern __shared__ __align__(16) unsigned char sec_smem[];
     SecSmem &P = *reinterpret_cast<SecSmem *>(sec_smem);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1033,10 +1065,8 @@ __global__ void __launch_bounds__(TB, 5) k_build_pack(const T *__restrict__ w, u
             u64 al;
             if (j + 1 < nH) al = (u64)P.HI[j + 1] + 1;
             else al = nxt == NONE64 ? (u64)item + 1 : nxt + 1;
-            RowT row;
-            row.tw = tw_store<T>(tw, avg);
-            row.alias = (AliasT)al;
-            rows[item] = row;
+            sink.put(item, tw_store<TwT>(tw, avg), al);
+            ++nput;
         }
         if (last_round) break;
         // the resolved lights form a prefix: the next round starts after it
@@ -1080,17 +1110,24 @@ __global__ void __launch_bounds__(TB, 5) k_build_pack(const T *__restrict__ w, u
             if (r != 0xFFFFu) {
                 const u32 s = P.LS[r];
                 const u64 al = s ? (u64)s : (dflt ? dflt : t0 + p + 1);
-                RowT row;
-                row.tw = (TwT)w[t0 + p];
-                row.alias = (AliasT)al;
-                rows[t0 + p] = row;
+                sink.put(t0 + p, (TwT)w[t0 + p], al);
+                ++nput;
             }
         }
     }
+    if constexpr (Sink::counts) {
+        __shared__ u32 s_put;
+        if (threadIdx.x == 0) s_put = 0;
+        __syncthreads();
+        const u32 wsum = __reduce_add_sync(0xffffffffu, nput);
+        if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(&s_put, wsum);
+        __syncthreads();
+        if (threadIdx.x == 0 && s_put) atomicAdd(sink.written, (unsigned long long)s_put);
+    }
 }
 
-template <typename T>
-int run_build(const void *wv, u64 n, double avg, void *rows, void *ws, cudaStream_t st)
+template <typename T, typename Sink>
+int run_build(const void *wv, u64 n, double avg, Sink sink, void *ws, cudaStream_t st)
 {
     const T *w = (const T *)wv;
     BuildWs W = carve(ws, n);
@@ -1114,9 +1151,8 @@ int run_build(const void *wv, u64 n, double avg, void *rows, void *ws, cudaStrea
     k_build_split<T><<<(unsigned)((W.nt + 1 + NW - 1) / NW), TB, 0, st>>>(w, n, avg, W, O);
     AK_LAUNCH_CHECK("k_build_split");
     const size_t smem = sizeof(SecSmem);
-    AK_SMEM_ATTR(k_build_pack<T>, (int)smem);
-    k_build_pack<T><<<(unsigned)(W.nt + 1), TB, smem, st>>>(w, n, avg, W, O,
-                                                           (typename RowOf<T>::type *)rows);
+    AK_SMEM_ATTR((k_build_pack<T, Sink>), (int)smem);
+    k_build_pack<T, Sink><<<(unsigned)(W.nt + 1), TB, smem, st>>>(w, n, avg, W, O, sink);
     AK_LAUNCH_CHECK("k_build_pack");
     return AK_OK;
 }
@@ -1146,13 +1182,38 @@ int ak_build_psa_avg(const void *w, int dtype, uint64_t n, double avg, void *row
     cudaStream_t st = ak_stream(stream);
     if (dtype == AK_F32) {
         if (n >= 0xFFFFFFFFull) return AK_ERR_VALUE;  // u32 aliases
-        return run_build<float>(w, n, avg, rows, ws, st);
+        return run_build<float>(w, n, avg, RowSink<float>{(RowF32 *)rows}, ws, st);
     }
     if (dtype == AK_F64) {
         if (n >= 0xFFFFFFFFull) return AK_ERR_VALUE;  // u32 item ids in the pack windows
-        return run_build<double>(w, n, avg, rows, ws, st);
+        return run_build<double>(w, n, avg, RowSink<double>{(RowF64 *)rows}, ws, st);
     }
     return AK_ERR_VALUE;
+}
+
+int ak_build_psa_residual(const double *res_w, uint64_t k, double avg, const int64_t *res_idx,
+                          int out_dtype, void *rows, uint64_t *written, void *ws, size_t ws_bytes,
+                          void *stream)
+{
+    *written = 0;
+    if (k == 0) return AK_OK;
+    if (ws_bytes < ws_bytes_for(k)) return AK_ERR_WORKSPACE;
+    if (((uintptr_t)res_w & 15) != 0 || k >= 0xFFFFFFFFull) return AK_ERR_VALUE;
+    if (out_dtype != AK_F32 && out_dtype != AK_F64) return AK_ERR_VALUE;
+    cudaStream_t st = ak_stream(stream);
+    unsigned long long *c = (unsigned long long *)ak_stream_scratch(st);
+    if (!c) return AK_ERR_CUDA;
+    int rc = ak_fill_small(c, 0, 8, st);
+    if (rc != AK_OK) return rc;
+    if (out_dtype == AK_F32)
+        rc = run_build<double>(res_w, k, avg, RemapSink<RowF32>{(RowF32 *)rows, res_idx, avg, c}, ws, st);
+    else
+        rc = run_build<double>(res_w, k, avg, RemapSink<RowF64>{(RowF64 *)rows, res_idx, avg, c}, ws, st);
+    if (rc != AK_OK) return rc;
+    unsigned long long h = 0;
+    rc = ak_readback(st, &h, c, sizeof(h));
+    *written = h;
+    return rc;
 }
 
 int ak_build_stats(const void *ws, uint64_t n, uint64_t *nl, uint64_t *nh, uint64_t *tiles,

@@ -5,8 +5,9 @@ psa_plus_construct, pack.py:280-305) on the device.
 items pairs its lights and heavies (when it holds at least
 ``min_pair_threshold`` of each) in the block-local sequential order and
 forwards the leftovers in item order.  ``psa_plus_construct`` then builds the
-residual with the fused PSA pipeline at the global average and scatters its
-rows into the table (ak_build_psa_avg + ak_residual_scatter).
+residual with the fused PSA pipeline at the global average, its rows written
+straight into the table through the residual's item ids
+(ak_build_psa_residual).
 """
 
 from __future__ import annotations
@@ -78,27 +79,25 @@ def psa_plus_construct(w: WeightSet, s: int = 64, block_size: int = 4096,
 
     The reference's closing check, every bucket written (pack.py:303-304),
     is made from counts instead of a pass over the table: the prepack counts
-    the rows it pairs, the residual scatter the rows it writes with a nonzero
-    alias, and the two sets are disjoint by construction — so the table is
-    not cleared first and not re-read afterwards."""
+    the rows it pairs, the residual build the rows it writes through res_idx,
+    and the two sets are disjoint by construction — so the table is not
+    cleared first and not re-read afterwards."""
     t, res_idx, res_w, nwritten = _prepack(w, block_size, threshold, clear_rows=False)
     k = res_idx.numel()
     dev = w.weights.device
     L = _lib.lib()
     if k:
-        rt = torch.empty(2 * k, dtype=torch.int64, device=dev)  # f64 rows over residual positions
+        # the residual built with the global average, its rows written
+        # straight into the table through res_idx (no intermediate table)
         ws = _lib.workspace(L.ak_build_workspace_bytes(k, _lib.F64), dev, "build")
         res_w = _lib.aligned32(res_w)
+        scattered = C.c_uint64(0)
         with torch.cuda.device(dev):
-            _lib.check(L.ak_build_psa_avg(_lib.ptr(res_w), _lib.F64, k, w.average, _lib.ptr(rt),
-                                          _lib.ptr(ws), ws.numel(), _lib.stream_ptr(dev)),
+            _lib.check(L.ak_build_psa_residual(_lib.ptr(res_w), k, w.average, _lib.ptr(res_idx),
+                                               t.dtype_code, _lib.ptr(t.rows), C.byref(scattered),
+                                               _lib.ptr(ws), ws.numel(), _lib.stream_ptr(dev)),
                        "psa_plus residual build")
-            scattered = C.c_uint64(0)
-            _lib.check(L.ak_residual_scatter_count(_lib.ptr(rt), _lib.ptr(res_idx), k, w.average,
-                                                   t.dtype_code, _lib.ptr(t.rows),
-                                                   C.byref(scattered), _lib.stream_ptr(dev)),
-                       "psa_plus residual scatter")
-            nwritten += int(scattered.value)
+        nwritten += int(scattered.value)
     if nwritten != w.n:
         raise PlanInconsistent("pack left buckets unwritten")
     return t

@@ -137,3 +137,41 @@ def test_psa_plus_large_handled_fraction(acceptance):
     ok = pre.handled_fraction >= 0.5 and rep.ok
     acceptance(f"{'PASS' if ok else 'FAIL'}  PSA+ N=1e7 uniform: handled {pre.handled_fraction:.4f}, {rep}")
     assert ok
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_fused_residual_build_equals_build_then_scatter(rng, dtype):
+    """ak_build_psa_residual (the residual build writing final rows through
+    res_idx) equals ak_build_psa_avg into a residual table followed by
+    ak_residual_scatter_count, bit for bit, and counts every residual row."""
+    import ctypes as C
+    from paper_2106_12270_b200 import _lib
+    from paper_2106_12270_b200.prepack import _prepack
+    L = _lib.lib()
+    for trial in range(6):
+        n = int(np.exp(rng.uniform(np.log(2000), np.log(2_000_000))))
+        w = random_weights(rng, n, trial % 5)
+        if dtype == torch.float32:
+            w = w.astype(np.float32)
+        ws = ak.make_weight_set(torch.from_numpy(np.ascontiguousarray(w)).to(DEV))
+        t, res_idx, res_w, _ = _prepack(ws, 512, 8, clear_rows=True)
+        k = res_idx.numel()
+        assert k > 0
+        res_w = _lib.aligned32(res_w)
+        a = t.rows.clone()
+        b = t.rows.clone()
+        s = _lib.stream_ptr()
+        bw = _lib.workspace(L.ak_build_workspace_bytes(k, _lib.F64), ws.weights.device)
+        rt = torch.empty(2 * k, dtype=torch.int64, device=DEV)
+        _lib.check(L.ak_build_psa_avg(_lib.ptr(res_w), _lib.F64, k, ws.average, _lib.ptr(rt),
+                                      _lib.ptr(bw), bw.numel(), s))
+        c1 = C.c_uint64(0)
+        _lib.check(L.ak_residual_scatter_count(_lib.ptr(rt), _lib.ptr(res_idx), k, ws.average,
+                                               t.dtype_code, _lib.ptr(a), C.byref(c1), s))
+        c2 = C.c_uint64(0)
+        _lib.check(L.ak_build_psa_residual(_lib.ptr(res_w), k, ws.average, _lib.ptr(res_idx),
+                                           t.dtype_code, _lib.ptr(b), C.byref(c2),
+                                           _lib.ptr(bw), bw.numel(), s))
+        torch.cuda.synchronize()
+        assert c2.value == k == c1.value
+        assert torch.equal(a, b), (n, trial)

@@ -1,6 +1,6 @@
 """Time psa_construct (CUDA events, device-resident weights) at one size.
 
-    python tools/time_build.py [--n 1e9] [--dist uniform|zipf] [--dtype float32|float64] [--reps 10]
+    python tools/time_build.py [--n 1e9] [--dist uniform|zipf] [--alpha 1.0] [--dtype float32|float64] [--reps 10]
                                [--method psa|psa_plus]
 """
 import argparse
@@ -17,13 +17,14 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=float, default=1e9)
 ap.add_argument("--dist", default="uniform")
 ap.add_argument("--dtype", default="float32")
+ap.add_argument("--alpha", type=float, default=1.0, help="power-law exponent for --dist zipf")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--method", default="psa")
 a = ap.parse_args()
 N = int(a.n)
 dt = torch.float32 if a.dtype == "float32" else torch.float64
 r = ak.RngStream(1)
-ws = ak.gen_uniform(N, r, dtype=dt) if a.dist == "uniform" else ak.gen_power_law(N, 1.0, r, dtype=dt)
+ws = ak.gen_uniform(N, r, dtype=dt) if a.dist == "uniform" else ak.gen_power_law(N, a.alpha, r, dtype=dt)
 t = build_table(ws)
 if a.method == "psa_plus":
     def build_table(ws, t):  # noqa: F811
@@ -43,5 +44,6 @@ ts.sort()
 b = 4 if dt == torch.float32 else 8
 byts = N * (2 * b + 2 * b)  # read w twice + write the row (8 B f32 / 16 B f64)
 med = ts[len(ts) // 2]
-print(f"{a.method} N={N:.0e} {a.dist} {a.dtype}: median {med:.3f} ms  min {ts[0]:.3f} ms  "
+dist = a.dist if a.dist == "uniform" else f"{a.dist}(alpha={a.alpha:g})"
+print(f"{a.method} N={N:.0e} {dist} {a.dtype}: median {med:.3f} ms  min {ts[0]:.3f} ms  "
       f"{N / med / 1e6:.1f} G items/s  {byts / med / 1e6:.0f} GB/s algorithmic")
