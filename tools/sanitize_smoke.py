@@ -33,6 +33,9 @@ for n, kind in ((1, 0), (7, 0), (2049, 1), (70_001, 0), (70_001, 2), (60_000, 3)
         ak.pack_section(p, plan, 1, ak.AliasTable.blank(n, ws.total, ws.dtype))
         tp = ak.psa_plus_construct(ws, block_size=64, threshold=4)
         assert tp.count_unwritten() == 0
+        if n > 40_000:  # > 2048 blocks: several chunks in the residual-count scan
+            tp = ak.psa_plus_construct(ws, block_size=16, threshold=2)
+            assert tp.count_unwritten() == 0
         x = ak.sample_batch(t, 5000, ak.RngStream(3, 1), rng="reference")
         y = ak.sectioned_sample(t, 64, 5000, ak.RngStream(3, 2), rng="philox4x32")
         z = ak.sectioned_sample(t, 64, 5000, ak.RngStream(3, 2), rng="reference")
