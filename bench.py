@@ -585,8 +585,13 @@ def run_ours(a):
                          "frac": ach / peak, "traffic": traffic,
                          "traffic_source": traffic_src if traffic else None, "kernel": "k_sample_sectioned",
                          "algorithmic_bytes_per_launch": pass_bytes, "peak_kind": peak_kind},
+            # PSA+ reads the weights once (the prepack) and writes each row
+            # once: N (b_w + b_row) algorithmic bytes; the residual's own
+            # build traffic counts against it
             "build_psa_plus": {"items_per_s": N / t_plus, "ms": t_plus * 1e3,
-                               "frac": build_bytes / t_plus / 1e9 / peak},
+                               "frac": N * (b_w + b_row) / t_plus / 1e9 / peak,
+                               "bytes_per_item": b_w + b_row,
+                               "speedup_vs_psa": t_build1 / t_plus},
             "sampling_reference_rng": {"samples_per_s": d0 / t_pass_ref,
                                        "frac": pass_bytes / t_pass_ref / 1e9 / peak},
             "e2e": e2e,
