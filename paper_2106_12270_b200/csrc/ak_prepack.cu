@@ -41,6 +41,21 @@ struct BlockInfo {
     u64 nwritten;   // rows written by the block
 };
 
+// a T at a shared-space address
+template <typename T> __device__ __forceinline__ T lds_at(u32 a);
+template <> __device__ __forceinline__ float lds_at<float>(u32 a)
+{
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+template <> __device__ __forceinline__ double lds_at<double>(u32 a)
+{
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+
 template <typename T> __device__ __forceinline__ int item_class(T v, double avg)
 {
     const double d = (double)v;
@@ -405,6 +420,13 @@ __global__ void __launch_bounds__(PPTB<T>::v) k_prepack_block(const T *__restric
                 }
                 u32 k = lo, j = d0 - lo;
                 const u32 steps = d0 + per < total ? per : total - d0;
+                // loop invariants kept in registers: the staged weights'
+                // shared-space address (opaque to the compiler, which would
+                // otherwise re-derive the dynamic shared base every step) and
+                // the block's first row
+                u32 sw_sa = (u32)__cvta_generic_to_shared(S.sw);
+                asm("" : "+r"(sw_sa));
+                RowT *const rb = rows + b0;
                 // one row per step on a single (branch-free) path: a taken
                 // heavy j closes against DL(k), a taken light k aliases heavy j
                 double dh = j < nh ? DH(j) : 0.0, dl = DL(k < nl ? k : nl);
@@ -418,9 +440,9 @@ __global__ void __launch_bounds__(PPTB<T>::v) k_prepack_block(const T *__restric
                     // step passes avg, as tw_store walks values above avg down
                     const TwT hv = tw_store<T>(take_h && wr ? (dh - dl) + avg : avg, avg);
                     RowT row;
-                    row.tw = take_h ? hv : (TwT)S.sw[it];
+                    row.tw = take_h ? hv : (TwT)lds_at<T>(sw_sa + it * (u32)sizeof(T));
                     row.alias = (AliasT)(b0 + al + 1);
-                    if (wr) rows[b0 + it] = row;
+                    if (wr) rb[it] = row;
                     if (take_h) {
                         ++j;
                         dh = j < nh ? DH(j) : 0.0;
