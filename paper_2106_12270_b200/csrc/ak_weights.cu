@@ -188,43 +188,61 @@ __global__ void __launch_bounds__(PW_WARPS * 32) k_pairwise_leaves(const T *__re
     }
     const Node mine = node_below(nd, PW_SLOT_DEPTH, (u32)lane);  // a leaf or nothing
     const u32 myoff = (u32)(mine.off - nd.off), mylen = mine.exists ? (u32)mine.size : 0u;
+    // the slots that hold a leaf, in order: a node's leaves sit above depth 5
+    // on every path where the sizes reach 128 early (at N=1e9 a ~1900-value
+    // node has 16 leaves of ~119 values in its 32 slots), so the groups walk
+    // the leaf list, not the slots
+    const unsigned leafm = __ballot_sync(0xffffffffu, mine.exists);
+    const int nleaf = __popc(leafm);
+    const int myrank = __popc(leafm & ((1u << lane) - 1u));
+    // lane r < nleaf: the slot of leaf r, the largest p with r set bits below it
+    int leafslot = 0;
+#pragma unroll
+    for (int b = 16; b >= 1; b >>= 1) {
+        const int c = leafslot + b;
+        if (__popc(leafm & (c >= 32 ? 0xffffffffu : (1u << c) - 1u)) <= lane) leafslot = c;
+    }
     const int g = lane >> 3, k = lane & 7;
     u64 bad = ~0ull;
     double leafsum = 0.0;
-    for (int s0 = 0; s0 < 32; s0 += 4) {
-        const int sl = s0 + g;  // slot handled by this group
-        const u32 off = __shfl_sync(0xffffffffu, myoff, sl);
-        const u32 len = __shfl_sync(0xffffffffu, mylen, sl);
+    for (int s0 = 0; s0 < nleaf; s0 += 4) {
+        const int j = s0 + g;  // leaf handled by this group
+        const int sl = __shfl_sync(0xffffffffu, leafslot, j & 31);
+        u32 off = __shfl_sync(0xffffffffu, myoff, sl);
+        u32 len = __shfl_sync(0xffffffffu, mylen, sl);
+        if (j >= nleaf) len = 0;
         const u64 base = nd.off + off;
         const u32 m8 = len >= 8 ? len - len % 8 : 0;
-        // all (<= 16) loads of the accumulator first, then its additions in order
-        double x[PW_BLOCK / 8];
+        // all (<= 16) loads of the accumulator first (kept in the input
+        // type), then its additions in order
+        T x[PW_BLOCK / 8];
 #pragma unroll
         for (int q = 0; q < (int)(PW_BLOCK / 8); ++q) {
             const u32 i = 8u * q + k;
-            x[q] = i < m8 ? ld_val(w, base + i) : 1.0;
+            x[q] = i < m8 ? __ldg(w + base + i) : T(1);
         }
         const u32 nt = len - m8;  // tail values (< 8), lane k holds tail value k
         const double xt = (u32)k < nt ? ld_val(w, base + m8 + k) : 1.0;
         double r = 0.0;
         if (len >= 8) {
-            r = x[0];
+            r = (double)x[0];
 #pragma unroll
             for (int q = 1; q < (int)(PW_BLOCK / 8); ++q)
-                if (8u * q < m8) r += x[q];
+                if (8u * q < m8) r += (double)x[q];
         }
         // finite and > 0: a NaN or inf makes the lane's sum non-finite and a
         // value <= 0 shows in the minimum; only then is the exact first bad
         // index searched for (a finite sum overflowing to inf just searches)
-        double mn = xt;
+        T mn = x[0];
 #pragma unroll
-        for (int q = 0; q < (int)(PW_BLOCK / 8); ++q) mn = fmin(mn, x[q]);
-        const bool ok = mn > 0.0 && isfinite(r + xt);
+        for (int q = 1; q < (int)(PW_BLOCK / 8); ++q) mn = mn < x[q] ? mn : x[q];
+        const bool ok = (double)mn > 0.0 && xt > 0.0 && isfinite(r + xt);
         if (!__all_sync(0xffffffffu, ok)) {
 #pragma unroll
             for (int q = 0; q < (int)(PW_BLOCK / 8); ++q) {
                 const u64 i = base + 8u * q + k;
-                if (!(x[q] > 0.0 && x[q] < CUDART_INF)) bad = bad < i ? bad : i;
+                const double xv = (double)x[q];
+                if (!(xv > 0.0 && xv < CUDART_INF)) bad = bad < i ? bad : i;
             }
             if (!(xt > 0.0 && xt < CUDART_INF)) bad = bad < base + m8 + k ? bad : base + m8 + k;
         }
@@ -234,13 +252,13 @@ __global__ void __launch_bounds__(PW_WARPS * 32) k_pairwise_leaves(const T *__re
         double res = s2 + __shfl_down_sync(0xffffffffu, s2, 4);
         if (len < 8) res = 0.0;
 #pragma unroll
-        for (int j = 0; j < 7; ++j) {  // the tail, in order
-            const double v = __shfl_sync(0xffffffffu, xt, (lane & ~7) + j);
-            if ((u32)j < nt) res += v;
+        for (int jj = 0; jj < 7; ++jj) {  // the tail, in order
+            const double v = __shfl_sync(0xffffffffu, xt, (lane & ~7) + jj);
+            if ((u32)jj < nt) res += v;
         }
-        // slot sl's sum -> lane sl
-        const double got = __shfl_sync(0xffffffffu, res, (lane & 3) * 8);
-        if ((lane >> 2) == (s0 >> 2)) leafsum = got;
+        // leaf j's sum -> the lane of its slot
+        const double got = __shfl_sync(0xffffffffu, res, ((myrank - s0) & 3) * 8);
+        if (mine.exists && myrank >= s0 && myrank < s0 + 4) leafsum = got;
     }
     // fold the 5 levels above the slots: node (lv, t) spans slots
     // [t 2^(5-lv), (t+1) 2^(5-lv)); its right child starts halfway
