@@ -10,7 +10,7 @@ C4  N=1e9 f32 table: one pass of batched/sectioned sampling (the bench's)
 C5  N=1e9 uniform f64 (and f32): construction; make_weight_set and PSA+
 Component operators of the reference API (partition_items, compute_split_plan,
 pack_all, partial_pary_search) on the C2 weights.
-Algorithmic bytes (SURVEY.md §8d): build N(2 b_w + b_row); naive M(b_row + 8);
+Algorithmic bytes (SURVEY.md §8d): build N(2 b_w + b_row), b_row 8 (f32) / 16 (f64); naive M(b_row + 8);
 sectioned M*8 + rows of the sections drawn.
 """
 import argparse
@@ -56,7 +56,8 @@ def build_row(name, n, dist, dtype, out):
     t = build_table(ws)
     s = timed(lambda: build_table(ws, t))
     bw = 4 if dtype == torch.float32 else 8
-    byts = n * (2 * bw + bw + 4)
+    brow = 8 if dtype == torch.float32 else 16  # (f32, u32) / (f64, u64) rows
+    byts = n * (2 * bw + brow)
     rep = ak.validate_table(t, ws, tol=1e-4 if dtype == torch.float32 else 1e-6,
                             row_tol=max(1e-9, 20 * n * 2.0**-53))
     out.append(dict(config=name, op=f"psa_construct N={n:.0e} {dist} {str(dtype)[6:]}", seconds=s,
@@ -118,7 +119,8 @@ def main():
                         rate_unit="items/s", gbs=10**9 * bw / s / 1e9, frac=10**9 * bw / s / 1e9 / PEAK,
                         parity="total bit-identical to np.sum: tests/test_gpu_core.py"))
         s = min(timed(lambda: ak.psa_plus_construct(wsd), reps=1) for _ in range(5))
-        byts = 10**9 * (3 * bw + 4)
+        # weights read once (the prepack) + each row written once
+        byts = 10**9 * (bw + (8 if dt == torch.float32 else 16))
         out.append(dict(config="C5", op=f"psa_plus_construct N=1e9 {str(dt)[6:]} (block 4096)", seconds=s,
                         rate=10**9 / s, rate_unit="items/s", gbs=byts / s / 1e9, frac=byts / s / 1e9 / PEAK,
                         parity="oracle PSA+ composition: tests/test_gpu_prepack.py"))
