@@ -175,3 +175,36 @@ def test_fused_residual_build_equals_build_then_scatter(rng, dtype):
         torch.cuda.synchronize()
         assert c2.value == k == c1.value
         assert torch.equal(a, b), (n, trial)
+
+
+def test_psa_plus_1e8_vs_oracle(acceptance):
+    """PSA+ at N=1e8 (f32 uniform, the bench's block size and threshold)
+    against the oracle's full composition: the block pass (partition.py:
+    134-282) and the residual PSA (pack.py:296-305) — every alias, and the
+    thresholds of rows with equal aliases within 1e-6 avg (f32 rows)."""
+    ws = ak.gen_uniform(10**8, ak.RngStream(seed=5), dtype=torch.float32)
+    w64 = ws.weights.double().cpu().numpy()
+    t = ak.psa_plus_construct(ws, block_size=4096, threshold=8)
+    pre, rtw, ral = oracle_psa_plus(w64, ws.total, 64, 4096, 8)
+    tw, al = t.to_numpy()
+    diff = int(np.count_nonzero(al != ral))
+    same = al == ral
+    worst = float(np.max(np.abs(tw - rtw)[same]) / ws.average)
+    rep = ak.validate_table(t, ws, tol=1e-4)
+    ok = diff == 0 and worst <= 1e-6 and rep.ok and t.count_unwritten() == 0
+    acceptance(f"{'PASS' if ok else 'FAIL'}  PSA+ N=1e8 f32 vs oracle composition: handled "
+               f"{pre['nwritten'] / w64.size:.4f}, alias diffs {diff}, worst |dtw| {worst:.1e} avg, {rep}")
+    assert ok
+
+
+def test_psa_plus_1e9_properties(acceptance):
+    """PSA+ on the bench's N=1e9 f32 weights: every bucket written (counted by
+    a pass over the table, independently of the construction's own counts),
+    per-item mass within the f32 bound, most items paired block-locally."""
+    ws = ak.gen_uniform(10**9, ak.RngStream(seed=1), dtype=torch.float32)
+    t = ak.psa_plus_construct(ws)
+    unwritten = t.count_unwritten()
+    rep = ak.validate_table(t, ws, tol=1e-4)
+    ok = unwritten == 0 and rep.ok
+    acceptance(f"{'PASS' if ok else 'FAIL'}  PSA+ N=1e9 f32: unwritten {unwritten}, {rep}")
+    assert ok
