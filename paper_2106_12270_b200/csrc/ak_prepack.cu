@@ -113,11 +113,16 @@ template <typename T> __device__ __forceinline__ PPSmem<T> pp_smem(unsigned char
 // prefixes took 54% of the kernel; this is 9.4 -> 7.6 ms at N=1e9 f32.
 // threads per prepack block: each owns P consecutive items read as 16-byte
 // vectors; 512 threads for f64 keep P = 8 (64 B per thread, the f32 pattern)
+// minb: CTAs per SM the register budget must allow.  Shared memory holds
+// f32 blocks to 3 CTAs/SM (61 KB each) and f64 blocks to 2 (77 KB); f32 at
+// minb 1 gets 77 registers (3 x 256 threads still fit), f64 at minb 2 gets
+// 64 (at minb 1 it took 88 and ran 1 CTA/SM: 15.9 ms against 11.0).
 template <typename T> struct PPTB {
     static constexpr int v = sizeof(T) == 4 ? 256 : 512;
+    static constexpr int minb = sizeof(T) == 4 ? 1 : 2;
 };
 template <typename T>
-__global__ void __launch_bounds__(PPTB<T>::v) k_prepack_block(const T *__restrict__ w, u64 n, double avg,
+__global__ void __launch_bounds__(PPTB<T>::v, PPTB<T>::minb) k_prepack_block(const T *__restrict__ w, u64 n, double avg,
                                                          u32 bs, u32 thr,
                                                          typename RowOf<T>::type *__restrict__ rows,
                                                          BlockInfo *__restrict__ info)
