@@ -15,11 +15,13 @@
  *   - `stream` is a cudaStream_t (may be NULL = legacy default stream); calls
  *     are stream-ordered and asynchronous unless marked [sync];
  *   - scratch comes from a caller workspace sized by a *_workspace_bytes
- *     query; the library never frees caller memory.  Its only state is a
- *     256-byte status buffer per (host thread, device, stream) for the
- *     [sync] entry points that read back a flag or count (allocated on first
- *     use, freed at thread exit); the device-attribute and kernel-attribute
- *     set-up is done once per process;
+ *     query; the library never frees caller memory.  Its only state, per
+ *     (host thread, device, stream), is a 256-byte device status buffer and
+ *     a 256-byte mapped pinned host mailbox for the [sync] entry points that
+ *     read back a flag or count (a one-block kernel writes the result into
+ *     the mailbox, so a readback never queues behind bulk copies on the copy
+ *     engines; both allocated on first use, freed at thread exit); the
+ *     device-attribute and kernel-attribute set-up is done once per process;
  *   - every function returns an ak_status; Python wrappers map the codes 1:1
  *     onto the reference exceptions (model.py:32-46, split.py:28-33,
  *     pack.py:26-27, sample.py:40-41, stats.py:17-22).
