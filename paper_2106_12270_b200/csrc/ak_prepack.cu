@@ -123,7 +123,7 @@ template <typename T> struct PPTB {
 };
 template <typename T>
 __global__ void __launch_bounds__(PPTB<T>::v, PPTB<T>::minb) k_prepack_block(const T *__restrict__ w, u64 n, double avg,
-                                                         u32 bs, u32 thr,
+                                                         u32 bs, u32 thr, u32 pf_ahead,
                                                          typename RowOf<T>::type *__restrict__ rows,
                                                          BlockInfo *__restrict__ info)
 {
@@ -135,7 +135,6 @@ __global__ void __launch_bounds__(PPTB<T>::v, PPTB<T>::minb) k_prepack_block(con
     const PPSmem<T> S = pp_smem<T>(pp_raw, bs);
     __shared__ u64 s_written;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const u32 lt = (1u << lane) - 1u;
     const u64 b0 = (u64)blockIdx.x * bs;
     const u32 len = (u32)(b0 + bs <= n ? bs : n - b0);
     // stage the block's weights: one bulk async copy (TMA) when aligned
@@ -150,6 +149,14 @@ __global__ void __launch_bounds__(PPTB<T>::v, PPTB<T>::minb) k_prepack_block(con
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             mbar_expect_tx(&bar, bytes);
             bulk_g2s(S.sw, src, bytes, &bar);
+        }
+        // warm L2 with the weights of the block that starts about one
+        // resident grid later, so its own bulk copy hits L2
+        const u64 pb = (u64)blockIdx.x + pf_ahead;
+        if (pf_ahead && (pb + 1) * bs <= n) {
+            const T *pf = w + pb * bs;
+            if ((((uintptr_t)pf) & 15) == 0 && ((bs * (u32)sizeof(T)) & 15) == 0)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"(bs * (u32)sizeof(T)) : "memory");
         }
     }
     if (bulk) {
@@ -669,6 +676,22 @@ size_t pp_smem_bytes(u32 bs, size_t wb) { return (((size_t)bs * wb + 15) & ~(siz
 
 inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// blocks resident at once (SMs x CTAs per SM): how far ahead a block warms
+// L2 for its successor on the same SM slot
+#ifndef PP_PREFETCH
+#define PP_PREFETCH 1
+#endif
+u32 pp_prefetch_distance(const void *kern, int threads, size_t smem)
+{
+    if (!PP_PREFETCH) return 0;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return 0;
+    }
+    return (u32)(per_sm * ak_num_sms());
+}
+
 }  // namespace
 
 extern "C" int ak_build_psa_avg(const void *w, int dtype, uint64_t n, double avg, void *rows,
@@ -720,12 +743,14 @@ int ak_greedy_prepack_ex(const void *w, int dtype, uint64_t n, double avg, uint3
     }
     if (dtype == AK_F32) {
         AK_SMEM_ATTR(k_prepack_block<float>, (int)smem);
-        k_prepack_block<float><<<(unsigned)nb, PPTB<float>::v, smem, st>>>((const float *)w, n, avg, block_size,
-                                                                 threshold, (RowF32 *)rows, info);
+        k_prepack_block<float><<<(unsigned)nb, PPTB<float>::v, smem, st>>>(
+            (const float *)w, n, avg, block_size, threshold,
+            pp_prefetch_distance((const void *)k_prepack_block<float>, PPTB<float>::v, smem), (RowF32 *)rows, info);
     } else if (dtype == AK_F64) {
         AK_SMEM_ATTR(k_prepack_block<double>, (int)smem);
-        k_prepack_block<double><<<(unsigned)nb, PPTB<double>::v, smem, st>>>((const double *)w, n, avg, block_size,
-                                                                  threshold, (RowF64 *)rows, info);
+        k_prepack_block<double><<<(unsigned)nb, PPTB<double>::v, smem, st>>>(
+            (const double *)w, n, avg, block_size, threshold,
+            pp_prefetch_distance((const void *)k_prepack_block<double>, PPTB<double>::v, smem), (RowF64 *)rows, info);
     } else {
         return AK_ERR_VALUE;
     }
