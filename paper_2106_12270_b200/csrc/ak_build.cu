@@ -254,28 +254,6 @@ __device__ __forceinline__ dd shfl_xor_dd(dd x, int m)
     return dd_make(__shfl_xor_sync(0xffffffffu, x.hi, m), __shfl_xor_sync(0xffffffffu, x.lo, m));
 }
 
-// Reduce-scatter of eight per-lane values over the warp: lane l returns the
-// warp sum of value l >> 2 (3 halving exchanges + 2 butterfly steps).
-__device__ __forceinline__ double reduce8(const double v[NW], int lane)
-{
-    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-    double a[4], b[2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const double keep = b4 ? v[4 + i] : v[i], send = b4 ? v[i] : v[4 + i];
-        a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const double keep = b3 ? a[2 + i] : a[i], send = b3 ? a[i] : a[2 + i];
-        b[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    double c = (b2 ? b[1] : b[0]) + __shfl_xor_sync(0xffffffffu, b2 ? b[0] : b[1], 4);
-    c = c + __shfl_xor_sync(0xffffffffu, c, 2);
-    c = c + __shfl_xor_sync(0xffffffffu, c, 1);
-    return c;
-}
-
 // lane's 8 items of a chunk staged in shared memory (T values, not widened)
 template <typename T>
 __device__ __forceinline__ void lds8_raw(const T *p, T v[VV])
@@ -426,7 +404,7 @@ __global__ void __launch_bounds__(SC_WARPS * 32) k_build_scan(const T *__restric
         // chunk totals -> lanes 0..7, then their monotone scan -> chunk bounds
         // chunk totals: lane l sums lanes 8q..8q+7 of chunk l>>2 (q = l&3)
         // for both classes, two butterfly steps finish: lanes 4c..4c+3 hold
-        // chunk c's totals (the reduce-scatter layout of reduce8)
+        // chunk c's totals (a reduce-scatter layout)
         __syncwarp();
         double rD, rE;
         {
@@ -877,7 +855,7 @@ template <typename RowOut> struct RemapSink {
 
 template <typename T, typename Sink>
 __global__ void __launch_bounds__(TB, 5) k_build_pack(const T *__restrict__ w, u64 n, double avg,
-                                                      BuildWs W, SplitOut O, Sink sink)
+                                                      BuildWs W, SplitOut O, Sink sink, u32 pf_ahead)
 {
     typedef typename Sink::TwT TwT;
     u32 nput = 0;  // rows written by this thread (RemapSink counts them)
@@ -891,6 +869,20 @@ __global__ void __launch_bounds__(TB, 5) k_build_pack(const T *__restrict__ w, u
     const dd own = u < nt ? W.DLb[u] : W.DLb[nt];
     const double secbound = u < nt ? W.mD[u * NW + NW - 1] : 0.0;  // next light key, own frame
 
+    if (threadIdx.x == 0 && pf_ahead) {
+        // warm L2 for the section one resident grid ahead: its tile and the
+        // start of its heavy window (so its loads hit L2, not DRAM)
+        const u64 v = blockIdx.x + (u64)pf_ahead;
+        if (v < W.nt && (v + 1) * TILE <= n)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(w + v * TILE),
+                         "r"((u32)(TILE * sizeof(T))) : "memory");
+        if (v < W.nt) {
+            const u64 g = O.hchunk[v];
+            if ((g + 8) * CH <= n)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(w + g * CH),
+                             "r"((u32)(8 * CH * sizeof(T))) : "memory");
+        }
+    }
     // ---- lights of tile u (rank order = key order), keys into shared memory
     reinterpret_cast<uint4 *>(P.LS)[threadIdx.x] = make_uint4(0, 0, 0, 0);
     reinterpret_cast<uint4 *>(P.LS)[threadIdx.x + TB] = make_uint4(0, 0, 0, 0);
@@ -1152,7 +1144,15 @@ int run_build(const void *wv, u64 n, double avg, Sink sink, void *ws, cudaStream
     AK_LAUNCH_CHECK("k_build_split");
     const size_t smem = sizeof(SecSmem);
     AK_SMEM_ATTR((k_build_pack<T, Sink>), (int)smem);
-    k_build_pack<T, Sink><<<(unsigned)(W.nt + 1), TB, smem, st>>>(w, n, avg, W, O, sink);
+    u32 pf = 0;
+    {
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_build_pack<T, Sink>, TB, smem) == cudaSuccess)
+            pf = (u32)(per_sm * ak_num_sms());
+        else
+            (void)cudaGetLastError();
+    }
+    k_build_pack<T, Sink><<<(unsigned)(W.nt + 1), TB, smem, st>>>(w, n, avg, W, O, sink, pf);
     AK_LAUNCH_CHECK("k_build_pack");
     return AK_OK;
 }
