@@ -45,7 +45,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=float, default=1e9)
+    # --items: the spelling to use under torchrun (its parser takes "--n" for
+    # an abbreviation of its own --nnodes / --nproc-per-node)
+    ap.add_argument("--items", "--n", dest="n", type=float, default=1e9)
     ap.add_argument("--samples", type=float, default=1e11, help="draws per step per GPU (weak scaling)")
     ap.add_argument("--section", type=int, default=1 << 14)
     ap.add_argument("--rng", default="philox4x32", choices=["philox4x32", "reference"])
@@ -59,6 +61,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-f64", action="store_true", help="skip the C5 float64 build/sampling legs")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N>1 process-group backend; gloo lets several ranks share one GPU "
+                         "(a functional check of the multi-rank path; numbers are not scaling data)")
     ap.add_argument("--broadcast", action="store_true",
                     help="N>1: rank 0 builds the table and NCCL-broadcasts it every step "
                          "(instead of every rank rebuilding it from the replicated weights)")
@@ -255,10 +260,15 @@ def run_ours(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.dist_backend == "gloo":
+        local = local % torch.cuda.device_count()  # ranks may share a GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if a.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     N = int(a.n)
     M = int(a.samples)
     S = a.section
@@ -601,7 +611,8 @@ def run_ours(a):
             "c5_float64": f64,
             "cpu_baseline": cpu,
             "table_broadcast": bcast,
-            "step_variant": ("rank 0 builds, NCCL broadcast of the table every step" if bcast_step
+            "dist_backend": a.dist_backend if world > 1 else None,
+            "step_variant": (f"rank 0 builds, {a.dist_backend.upper()} broadcast of the table every step" if bcast_step
                              else "every rank rebuilds the table from its replicated weights"),
             # per step: the build (2 scratch fills + scan, coarse split, split, pack)
             # and one sectioned-sampling launch per pass

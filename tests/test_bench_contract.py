@@ -65,3 +65,27 @@ def test_reference_arm_weights_match_gpu_arm():
     host = bench.reference_weights(n)
     dev = ak.gen_uniform(n, ak.RngStream(seed=1), dtype=torch.float32).weights.double().cpu().numpy()
     assert np.array_equal(host, dev)
+
+
+@pytest.mark.gpu
+def test_two_rank_bench_line_under_torchrun():
+    """The driver's N>1 launch (torch.distributed.run, one process per rank)
+    end to end: barriers, max-over-ranks timing, the whole-job value, the
+    e2e split across ranks and the broadcast step variant.  Two ranks share
+    one GPU over gloo (NCCL needs a GPU per rank), so this checks the
+    multi-rank code path, not scaling."""
+    for extra in ([], ["--broadcast"]):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+               "--master-addr", "127.0.0.1", "--master-port", str(29600 + len(extra)),
+               os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dist-backend", "gloo",
+               "--items", "1e7", "--samples", "2e8", "--steps", "2", "--warmup", "3", "--no-cpu",
+               "--e2e-samples", "4e7", "--e2e-steps", "1"] + extra
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+        assert r.returncode == 0, r.stderr[-3000:]
+        lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        assert len(lines) == 1, r.stdout[-2000:]  # rank 0 alone prints
+        d = json.loads(lines[0])
+        assert KEYS <= set(d) and d["n_gpus"] == 2 and d["scaling"] == "weak"
+        assert d["config"]["samples_total"] == 2 * d["config"]["samples_per_gpu"]
+        assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["table_broadcast"]["bytes"] > 0
+        assert ("broadcast" in d["step_variant"]) == bool(extra)
