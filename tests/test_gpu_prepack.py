@@ -177,12 +177,16 @@ def test_fused_residual_build_equals_build_then_scatter(rng, dtype):
         assert torch.equal(a, b), (n, trial)
 
 
-def test_psa_plus_1e8_vs_oracle(acceptance):
-    """PSA+ at N=1e8 (f32 uniform, the bench's block size and threshold)
-    against the oracle's full composition: the block pass (partition.py:
-    134-282) and the residual PSA (pack.py:296-305) — every alias, and the
-    thresholds of rows with equal aliases within 1e-6 avg (f32 rows)."""
-    ws = ak.gen_uniform(10**8, ak.RngStream(seed=5), dtype=torch.float32)
+@pytest.mark.parametrize("dtype,dist", [(torch.float32, "uniform"), (torch.float64, "uniform"),
+                                        (torch.float32, "zipf0.5")])
+def test_psa_plus_1e8_vs_oracle(dtype, dist, acceptance):
+    """PSA+ at N=1e8 (the bench's block size and threshold; uniform, and the
+    shuffled power law alpha=0.5 of the paper's second PSA+ case) against the
+    oracle's full composition: the block pass (partition.py:134-282) and the
+    residual PSA (pack.py:296-305) — every alias, and the thresholds of rows
+    with equal aliases within 1e-6 avg (f32 rows) / 1e-9 avg (f64 rows)."""
+    r = ak.RngStream(seed=5)
+    ws = ak.gen_uniform(10**8, r, dtype=dtype) if dist == "uniform" else ak.gen_power_law(10**8, 0.5, r, dtype=dtype)
     w64 = ws.weights.double().cpu().numpy()
     t = ak.psa_plus_construct(ws, block_size=4096, threshold=8)
     pre, rtw, ral = oracle_psa_plus(w64, ws.total, 64, 4096, 8)
@@ -190,9 +194,13 @@ def test_psa_plus_1e8_vs_oracle(acceptance):
     diff = int(np.count_nonzero(al != ral))
     same = al == ral
     worst = float(np.max(np.abs(tw - rtw)[same]) / ws.average)
-    rep = ak.validate_table(t, ws, tol=1e-4)
-    ok = diff == 0 and worst <= 1e-6 and rep.ok and t.count_unwritten() == 0
-    acceptance(f"{'PASS' if ok else 'FAIL'}  PSA+ N=1e8 f32 vs oracle composition: handled "
+    tol = 1e-6 if dtype == torch.float32 else 1e-9
+    # the row bound scaled with N as for PSA at this size (SURVEY.md §8c item
+    # 3: the reference's own Vose exceeds 1e-9 avg from N=1e7 on by chain drift)
+    rep = ak.validate_table(t, ws, tol=1e-4 if dtype == torch.float32 else 1e-9,
+                            row_tol=max(1e-9, 20 * 10**8 * 2.0**-53))
+    ok = diff == 0 and worst <= tol and rep.ok and t.count_unwritten() == 0
+    acceptance(f"{'PASS' if ok else 'FAIL'}  PSA+ N=1e8 {str(dtype)[6:]} {dist} vs oracle composition: handled "
                f"{pre['nwritten'] / w64.size:.4f}, alias diffs {diff}, worst |dtw| {worst:.1e} avg, {rep}")
     assert ok
 
