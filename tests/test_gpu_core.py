@@ -110,6 +110,18 @@ def test_weight_set_totals_bit_identical_to_np_sum(golden, rng):
         assert ws.total == float(np.sum(w32.astype(np.float64)))
 
 
+def test_weight_set_totals_sweep_tree_shapes(rng):
+    """np.sum's pairwise tree at 48 log-uniform sizes up to 1e8: the cut
+    nodes (about 1025..2048 values) reach leaves of <= 128 values at depth 4
+    or 5 depending on n, and the device walks each node's leaf list."""
+    sizes = sorted({int(x) for x in np.exp(rng.uniform(np.log(3e3), np.log(1e8), 48))})
+    for n in sizes:
+        for dt in (torch.float64, torch.float32):
+            w = (torch.rand(n, dtype=torch.float64, device=DEV) + 1e-3).to(dt)
+            expect = float(np.sum(w.cpu().numpy().astype(np.float64)))
+            assert ak.make_weight_set(w).total == expect, (n, dt)
+
+
 @pytest.mark.parametrize("bad,idx", [([1.0, 0.0, 2.0], 2), ([1.0, -3.0], 2),
                                      ([float("nan"), 1.0], 1), ([1.0, float("inf")], 2)])
 def test_invalid_weight_reports_1based_index(bad, idx):
