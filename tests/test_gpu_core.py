@@ -204,6 +204,23 @@ def test_partition_matches_reference(golden, hand):
             assert np.all(np.abs(got - want) <= 2 * ulp), f  # dd-exact vs Neumaier
 
 
+@pytest.mark.parametrize("n", [524_289, 3_000_017, 20_000_003])
+def test_partition_many_chunks_vs_oracle(rng, n):
+    """partition_items past one scan chunk (> 256 tiles of 2048 items): the
+    chunk scans + chained carries give the oracle's order exactly and its
+    Neumaier prefixes within 2 ulp (partition.py:62-131)."""
+    w = rng.pareto(1.1, n) + 1e-6
+    ws = ak.make_weight_set(torch.from_numpy(w).to(DEV))
+    p = ak.partition_items(ws)
+    po = O.partition_items(w, ws.total)
+    for f in ("l_index", "l_weight", "h_index", "h_weight"):
+        assert np.array_equal(getattr(p, f).cpu().numpy(), po[f]), f
+    for f in ("lprefix", "hprefix"):
+        got, want = getattr(p, f).cpu().numpy(), po[f]
+        ulp = np.spacing(np.maximum(np.abs(want), 1e-300))
+        assert np.all(np.abs(got - want) <= 2 * ulp), f
+
+
 def test_prefix_sums_recover_increments(rng):
     ws = ak.make_weight_set(rng.pareto(1.1, 30000) + 1e-6)
     p = ak.partition_items(ws)
