@@ -334,23 +334,32 @@ __global__ void __launch_bounds__(PPTB<T>::v, PPTB<T>::minb) k_prepack_block(con
         auto DL = [&](u32 k) { return key[pk(k)]; };           // [0, nl]
         auto DH = [&](u32 j) { return key[pk(nl + 1 + j)]; };  // [0, nh)
         // lights absorbed before the sweep stops: #lights with DL < DH(j)
-        auto lights_below = [&](double x) {
-            u32 a = 0, b = nl;  // first k with DL(k) >= x
-            while (a < b) {
-                const u32 m = (a + b) >> 1;
-                if (DL(m) < x) a = m + 1;
-                else b = m;
+        // first index in [0, cnt) satisfying a monotone (false .. true)
+        // predicate, cnt if none: a warp-cooperative 32-ary search (32 probes
+        // and a ballot per step, 3 steps for a 4096-item block), run by every
+        // warp on the same keys -- the binary search's answer without its 12
+        // dependent shared loads per thread
+        auto warp_first = [&](u32 cnt, auto pred) {
+            u32 lo = 0, hi = cnt;  // answer in [lo, hi]
+            while (hi - lo >= 32) {  // the last step's 32 probes then cover [lo, hi]
+                const u32 step = (hi - lo + 31) / 32;
+                const u32 q = lo + (lane + 1) * step - 1;
+                const unsigned m = __ballot_sync(0xffffffffu, q >= hi || pred(q));
+                if (!m) { lo = hi; break; }
+                const u32 f = (u32)__ffs(m) - 1;
+                const u32 qf = lo + (f + 1) * step - 1;
+                lo += f * step;
+                hi = qf < hi ? qf : hi;
             }
-            return a;
+            const u32 q = lo + lane;
+            const unsigned m = __ballot_sync(0xffffffffu, q >= hi || pred(q));
+            return lo + (u32)__ffs(m) - 1;
         };
-        auto heavies_upto = [&](double x) {
-            u32 a = 0, b = nh;  // first j with DH(j) > x
-            while (a < b) {
-                const u32 m = (a + b) >> 1;
-                if (DH(m) <= x) a = m + 1;
-                else b = m;
-            }
-            return a;
+        auto lights_below = [&](double x) {  // first k with DL(k) >= x
+            return warp_first(nl, [&](u32 k) { return DL(k) >= x; });
+        };
+        auto heavies_upto = [&](double x) {  // first j with DH(j) > x
+            return warp_first(nh, [&](u32 j) { return DH(j) > x; });
         };
         if (DH(nh - 1) <= DLtot) {
             jt = (int)nh - 1;
