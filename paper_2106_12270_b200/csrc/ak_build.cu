@@ -1132,14 +1132,7 @@ int run_build(const void *wv, u64 n, double avg, Sink sink, void *ws, cudaStream
     AK_LAUNCH_CHECK("k_build_split");
     const size_t smem = sizeof(SecSmem);
     AK_SMEM_ATTR((k_build_pack<T, Sink>), (int)smem);
-    u32 pf = 0;
-    {
-        int per_sm = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_build_pack<T, Sink>, TB, smem) == cudaSuccess)
-            pf = (u32)(per_sm * ak_num_sms());
-        else
-            (void)cudaGetLastError();
-    }
+    const u32 pf = ak_resident_ctas((const void *)k_build_pack<T, Sink>, TB, smem);  // queried once
     k_build_pack<T, Sink><<<(unsigned)(W.nt + 1), TB, smem, st>>>(w, n, avg, W, O, sink, pf);
     AK_LAUNCH_CHECK("k_build_pack");
     return AK_OK;

@@ -40,6 +40,7 @@ int ak_check_launch(const char *where);
 static inline cudaStream_t ak_stream(void *s) { return (cudaStream_t)s; }
 
 int ak_num_sms();
+unsigned ak_resident_ctas(const void *kernel, int threads, size_t smem);
 void *ak_stream_scratch(cudaStream_t st);  // 256 B per (host thread, device, stream)
 void *ak_mailbox(cudaStream_t st);         // 256 B mapped pinned host memory, same keying
 // Small device results (up to 3 pieces, <= 256 bytes in all) to host memory

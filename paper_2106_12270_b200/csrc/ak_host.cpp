@@ -11,6 +11,7 @@
 #include <utility>
 #include <map>
 #include <mutex>
+#include <tuple>
 #include <cuda_runtime.h>
 
 #include <cfenv>
@@ -115,6 +116,35 @@ cudaError_t ak_smem_attr_once(const void *kernel, int bytes)
     e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e == cudaSuccess) have = bytes;
     return e;
+}
+
+int ak_num_sms();
+
+// CTAs of `kernel` resident at once on the whole device (SMs x CTAs per SM)
+// for a block size and dynamic shared memory, queried once per (kernel,
+// device, threads, smem): the L2-prefetch distance of the construction
+// kernels, kept off the per-call path (0 if the query fails)
+unsigned ak_resident_ctas(const void *kernel, int threads, size_t smem)
+{
+    static std::mutex mu;
+    static std::map<std::tuple<const void *, int, int, size_t>, unsigned> cache;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    const auto key = std::make_tuple(kernel, dev, threads, smem);
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    int per_sm = 0;
+    unsigned v = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) == cudaSuccess)
+        v = (unsigned)(per_sm * ak_num_sms());
+    else
+        (void)cudaGetLastError();
+    std::lock_guard<std::mutex> g(mu);
+    cache[key] = v;
+    return v;
 }
 
 int ak_num_sms()

@@ -686,19 +686,10 @@ size_t pp_smem_bytes(u32 bs, size_t wb) { return (((size_t)bs * wb + 15) & ~(siz
 inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // blocks resident at once (SMs x CTAs per SM): how far ahead a block warms
-// L2 for its successor on the same SM slot
-#ifndef PP_PREFETCH
-#define PP_PREFETCH 1
-#endif
+// L2 for its successor on the same SM slot (queried once, ak_host.cpp)
 u32 pp_prefetch_distance(const void *kern, int threads, size_t smem)
 {
-    if (!PP_PREFETCH) return 0;
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess) {
-        (void)cudaGetLastError();
-        return 0;
-    }
-    return (u32)(per_sm * ak_num_sms());
+    return ak_resident_ctas(kern, threads, smem);
 }
 
 }  // namespace
