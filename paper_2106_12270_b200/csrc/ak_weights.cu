@@ -202,63 +202,133 @@ __global__ void __launch_bounds__(PW_WARPS * 32) k_pairwise_leaves(const T *__re
         const int c = leafslot + b;
         if (__popc(leafm & (c >= 32 ? 0xffffffffu : (1u << c) - 1u)) <= lane) leafslot = c;
     }
-    const int g = lane >> 3, k = lane & 7;
     u64 bad = ~0ull;
     double leafsum = 0.0;
-    for (int s0 = 0; s0 < nleaf; s0 += 4) {
-        const int j = s0 + g;  // leaf handled by this group
-        const int sl = __shfl_sync(0xffffffffu, leafslot, j & 31);
-        u32 off = __shfl_sync(0xffffffffu, myoff, sl);
-        u32 len = __shfl_sync(0xffffffffu, mylen, sl);
-        if (j >= nleaf) len = 0;
-        const u64 base = nd.off + off;
-        const u32 m8 = len >= 8 ? len - len % 8 : 0;
-        // all (<= 16) loads of the accumulator first (kept in the input
-        // type), then its additions in order
-        T x[PW_BLOCK / 8];
+    // f32 weights 8-byte aligned: float2 loads, 4 lanes per leaf (lane k of
+    // a group holds numpy's accumulators r_2k and r_2k+1), 8 leaves per pass.
+    // Leaves start at multiples of 8 (numpy splits at multiples of 8), so the
+    // pairs are aligned.  The additions are numpy's, in its order.
+    if (sizeof(T) == 4 && (((uintptr_t)w) & 7) == 0) {
+        const int g = lane >> 2, k = lane & 3;
+        for (int s0 = 0; s0 < nleaf; s0 += 8) {
+            const int j = s0 + g;  // leaf handled by this group
+            const int sl = __shfl_sync(0xffffffffu, leafslot, j & 31);
+            const u32 off = __shfl_sync(0xffffffffu, myoff, sl);
+            u32 len = __shfl_sync(0xffffffffu, mylen, sl);
+            if (j >= nleaf) len = 0;
+            const u64 base = nd.off + off;
+            const u32 m8 = len >= 8 ? len - len % 8 : 0;
+            const float2 *wp = reinterpret_cast<const float2 *>(reinterpret_cast<const float *>(w) + base);
+            float2 x[PW_BLOCK / 8];
 #pragma unroll
-        for (int q = 0; q < (int)(PW_BLOCK / 8); ++q) {
-            const u32 i = 8u * q + k;
-            x[q] = i < m8 ? __ldg(w + base + i) : T(1);
-        }
-        const u32 nt = len - m8;  // tail values (< 8), lane k holds tail value k
-        const double xt = (u32)k < nt ? ld_val(w, base + m8 + k) : 1.0;
-        double r = 0.0;
-        if (len >= 8) {
-            r = (double)x[0];
+            for (int q = 0; q < (int)(PW_BLOCK / 8); ++q)
+                x[q] = 8u * q < m8 ? __ldg(wp + 4 * q + k) : make_float2(1.f, 1.f);
+            const u32 nt = len - m8;  // tail values (< 8): lane k holds tail values 2k, 2k + 1
+            const double t0 = (u32)(2 * k) < nt ? ld_val(w, base + m8 + 2 * k) : 1.0;
+            const double t1 = (u32)(2 * k + 1) < nt ? ld_val(w, base + m8 + 2 * k + 1) : 1.0;
+            double ra = 0.0, rb = 0.0;
+            if (len >= 8) {
+                ra = (double)x[0].x;
+                rb = (double)x[0].y;
 #pragma unroll
-            for (int q = 1; q < (int)(PW_BLOCK / 8); ++q)
-                if (8u * q < m8) r += (double)x[q];
-        }
-        // finite and > 0: a NaN or inf makes the lane's sum non-finite and a
-        // value <= 0 shows in the minimum; only then is the exact first bad
-        // index searched for (a finite sum overflowing to inf just searches)
-        T mn = x[0];
-#pragma unroll
-        for (int q = 1; q < (int)(PW_BLOCK / 8); ++q) mn = mn < x[q] ? mn : x[q];
-        const bool ok = (double)mn > 0.0 && xt > 0.0 && isfinite(r + xt);
-        if (!__all_sync(0xffffffffu, ok)) {
-#pragma unroll
-            for (int q = 0; q < (int)(PW_BLOCK / 8); ++q) {
-                const u64 i = base + 8u * q + k;
-                const double xv = (double)x[q];
-                if (!(xv > 0.0 && xv < CUDART_INF)) bad = bad < i ? bad : i;
+                for (int q = 1; q < (int)(PW_BLOCK / 8); ++q)
+                    if (8u * q < m8) {
+                        ra += (double)x[q].x;
+                        rb += (double)x[q].y;
+                    }
             }
-            if (!(xt > 0.0 && xt < CUDART_INF)) bad = bad < base + m8 + k ? bad : base + m8 + k;
-        }
-        // ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7)) within the group
-        const double s1 = r + __shfl_down_sync(0xffffffffu, r, 1);
-        const double s2 = s1 + __shfl_down_sync(0xffffffffu, s1, 2);
-        double res = s2 + __shfl_down_sync(0xffffffffu, s2, 4);
-        if (len < 8) res = 0.0;
+            float mn = fminf(x[0].x, x[0].y);
 #pragma unroll
-        for (int jj = 0; jj < 7; ++jj) {  // the tail, in order
-            const double v = __shfl_sync(0xffffffffu, xt, (lane & ~7) + jj);
-            if ((u32)jj < nt) res += v;
+            for (int q = 1; q < (int)(PW_BLOCK / 8); ++q) {
+                mn = mn < x[q].x ? mn : x[q].x;
+                mn = mn < x[q].y ? mn : x[q].y;
+            }
+            const bool ok = x[0].x == x[0].x && x[0].y == x[0].y && (double)mn > 0.0 && t0 > 0.0 &&
+                            t1 > 0.0 && isfinite(ra + rb + t0 + t1);
+            if (!__all_sync(0xffffffffu, ok)) {
+#pragma unroll
+                for (int q = 0; q < (int)(PW_BLOCK / 8); ++q) {
+                    const u64 i = base + 8u * q + 2 * k;
+                    const double xa = (double)x[q].x, xb = (double)x[q].y;
+                    if (!(xa > 0.0 && xa < CUDART_INF)) bad = bad < i ? bad : i;
+                    if (!(xb > 0.0 && xb < CUDART_INF)) bad = bad < i + 1 ? bad : i + 1;
+                }
+                const u64 it = base + m8 + 2 * k;
+                if (!(t0 > 0.0 && t0 < CUDART_INF)) bad = bad < it ? bad : it;
+                if (!(t1 > 0.0 && t1 < CUDART_INF)) bad = bad < it + 1 ? bad : it + 1;
+            }
+            // ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7))
+            const double s = ra + rb;
+            const double s1 = s + __shfl_down_sync(0xffffffffu, s, 1);
+            double res = s1 + __shfl_down_sync(0xffffffffu, s1, 2);
+            if (len < 8) res = 0.0;
+#pragma unroll
+            for (int jj = 0; jj < 7; ++jj) {  // the tail, in order
+                const double va = __shfl_sync(0xffffffffu, t0, (lane & ~3) + (jj >> 1));
+                const double vb = __shfl_sync(0xffffffffu, t1, (lane & ~3) + (jj >> 1));
+                if ((u32)jj < nt) res += (jj & 1) ? vb : va;
+            }
+            // leaf j's sum -> the lane of its slot
+            const double got = __shfl_sync(0xffffffffu, res, ((myrank - s0) & 7) * 4);
+            if (mine.exists && myrank >= s0 && myrank < s0 + 8) leafsum = got;
         }
-        // leaf j's sum -> the lane of its slot
-        const double got = __shfl_sync(0xffffffffu, res, ((myrank - s0) & 3) * 8);
-        if (mine.exists && myrank >= s0 && myrank < s0 + 4) leafsum = got;
+    } else {
+        const int g = lane >> 3, k = lane & 7;
+        for (int s0 = 0; s0 < nleaf; s0 += 4) {
+            const int j = s0 + g;  // leaf handled by this group
+            const int sl = __shfl_sync(0xffffffffu, leafslot, j & 31);
+            u32 off = __shfl_sync(0xffffffffu, myoff, sl);
+            u32 len = __shfl_sync(0xffffffffu, mylen, sl);
+            if (j >= nleaf) len = 0;
+            const u64 base = nd.off + off;
+            const u32 m8 = len >= 8 ? len - len % 8 : 0;
+            // all (<= 16) loads of the accumulator first (kept in the input
+            // type), then its additions in order
+            T x[PW_BLOCK / 8];
+    #pragma unroll
+            for (int q = 0; q < (int)(PW_BLOCK / 8); ++q) {
+                const u32 i = 8u * q + k;
+                x[q] = i < m8 ? __ldg(w + base + i) : T(1);
+            }
+            const u32 nt = len - m8;  // tail values (< 8), lane k holds tail value k
+            const double xt = (u32)k < nt ? ld_val(w, base + m8 + k) : 1.0;
+            double r = 0.0;
+            if (len >= 8) {
+                r = (double)x[0];
+    #pragma unroll
+                for (int q = 1; q < (int)(PW_BLOCK / 8); ++q)
+                    if (8u * q < m8) r += (double)x[q];
+            }
+            // finite and > 0: a NaN or inf makes the lane's sum non-finite and a
+            // value <= 0 shows in the minimum; only then is the exact first bad
+            // index searched for (a finite sum overflowing to inf just searches)
+            T mn = x[0];
+    #pragma unroll
+            for (int q = 1; q < (int)(PW_BLOCK / 8); ++q) mn = mn < x[q] ? mn : x[q];
+            const bool ok = (double)mn > 0.0 && xt > 0.0 && isfinite(r + xt);
+            if (!__all_sync(0xffffffffu, ok)) {
+    #pragma unroll
+                for (int q = 0; q < (int)(PW_BLOCK / 8); ++q) {
+                    const u64 i = base + 8u * q + k;
+                    const double xv = (double)x[q];
+                    if (!(xv > 0.0 && xv < CUDART_INF)) bad = bad < i ? bad : i;
+                }
+                if (!(xt > 0.0 && xt < CUDART_INF)) bad = bad < base + m8 + k ? bad : base + m8 + k;
+            }
+            // ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7)) within the group
+            const double s1 = r + __shfl_down_sync(0xffffffffu, r, 1);
+            const double s2 = s1 + __shfl_down_sync(0xffffffffu, s1, 2);
+            double res = s2 + __shfl_down_sync(0xffffffffu, s2, 4);
+            if (len < 8) res = 0.0;
+    #pragma unroll
+            for (int jj = 0; jj < 7; ++jj) {  // the tail, in order
+                const double v = __shfl_sync(0xffffffffu, xt, (lane & ~7) + jj);
+                if ((u32)jj < nt) res += v;
+            }
+            // leaf j's sum -> the lane of its slot
+            const double got = __shfl_sync(0xffffffffu, res, ((myrank - s0) & 3) * 8);
+            if (mine.exists && myrank >= s0 && myrank < s0 + 4) leafsum = got;
+        }
     }
     // fold the 5 levels above the slots: node (lv, t) spans slots
     // [t 2^(5-lv), (t+1) 2^(5-lv)); its right child starts halfway
