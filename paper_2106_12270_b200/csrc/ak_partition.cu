@@ -28,9 +28,29 @@ struct PartAgg {
 template <typename T>
 __device__ __forceinline__ void load_tile(const T *w, u64 n, u64 base, double v[PT_V], bool ok[PT_V])
 {
+    const u64 i0 = base + (u64)threadIdx.x * PT_V;
+    if (i0 + PT_V <= n && ((((uintptr_t)(w + i0)) & 15) == 0)) {
+        // the thread's 8 consecutive values as 16-byte vector loads
+        if (sizeof(T) == 4) {
+            const float4 a = __ldg(reinterpret_cast<const float4 *>(w + i0));
+            const float4 b = __ldg(reinterpret_cast<const float4 *>(w + i0) + 1);
+            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+            v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+        } else {
+#pragma unroll
+            for (int q = 0; q < PT_V / 2; ++q) {
+                const double2 a = __ldg(reinterpret_cast<const double2 *>(w + i0) + q);
+                v[2 * q] = a.x;
+                v[2 * q + 1] = a.y;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < PT_V; ++k) ok[k] = true;
+        return;
+    }
 #pragma unroll
     for (int k = 0; k < PT_V; ++k) {
-        u64 i = base + (u64)threadIdx.x * PT_V + k;
+        u64 i = i0 + k;
         ok[k] = i < n;
         v[k] = ok[k] ? (double)w[i] : 0.0;
     }
