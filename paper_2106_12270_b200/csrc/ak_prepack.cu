@@ -19,12 +19,20 @@
 // Keys are block-local doubles (|key| <= block_size * avg), so decisions agree
 // with the reference's f64 chain except at ties inside its rounding noise.
 //
-//   k_prepack_block   classify (thread = P consecutive items), CTA scan,
-//                     compacted keys, merge, handled rows, per-block residual
-//                     summary
-//   k_prepack_emit    residual items (index, weight) in global item order
-//   k_residual_remap  the residual table (built by the fused builder with the
-//                     global average) scattered into the final table
+//   k_prepack_block   classify (thread = P consecutive items, branch-free),
+//                     CTA scan, compacted keys, the pairing decision (a
+//                     warp-cooperative 32-ary search), merge, handled rows,
+//                     per-block residual summary; warms L2 for the block one
+//                     resident grid ahead
+//   k_pp_partials / k_excl_scan_i64 / k_pp_offsets
+//                     the blocks' residual offsets (chunk sums, their scan,
+//                     chunk rescans)
+//   k_prepack_emit    residual items (index, weight) in global item order,
+//                     a warp per block
+//   k_residual_remap  a residual table scattered into the final table
+//                     (ak_residual_scatter; psa_plus_construct builds the
+//                     residual straight into the table instead,
+//                     ak_build_psa_residual in ak_build.cu)
 #include "ak_common.cuh"
 
 namespace {
@@ -110,7 +118,8 @@ template <typename T> __device__ __forceinline__ PPSmem<T> pp_smem(unsigned char
 // that writes the class-compacted keys and items; then one merge path over
 // the two key sequences writes every handled row (heavy first on ties:
 // DH <= DL).  Round 1's count pass + strided compaction + two in-place key
-// prefixes took 54% of the kernel; this is 9.4 -> 7.6 ms at N=1e9 f32.
+// prefixes took 54% of the kernel; this front half took it from 9.4 to
+// 7.6 ms at N=1e9 f32 (6.8 ms with the later changes listed above).
 // threads per prepack block: each owns P consecutive items read as 16-byte
 // vectors; 512 threads for f64 keep P = 8 (64 B per thread, the f32 pattern)
 // minb: CTAs per SM the register budget must allow.  Shared memory holds
