@@ -89,3 +89,13 @@ def test_two_rank_bench_line_under_torchrun():
         assert d["config"]["samples_total"] == 2 * d["config"]["samples_per_gpu"]
         assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["table_broadcast"]["bytes"] > 0
         assert ("broadcast" in d["step_variant"]) == bool(extra)
+
+
+def test_bench_options_parse_under_torchrun_spelling():
+    """--items (the spelling torchrun's own parser leaves alone) and --n set
+    the same value; --dist-backend accepts nccl and gloo (CPU-only check)."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--help"], capture_output=True,
+                       text=True, timeout=120, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "--items" in r.stdout and "--n" in r.stdout and "--dist-backend" in r.stdout
+    assert "gloo" in r.stdout
